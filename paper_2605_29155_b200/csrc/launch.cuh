@@ -1,0 +1,193 @@
+// launch.cuh — host-side launch planning for the DiffMPC kernels (shared by the
+// per-model instantiation units inst_*.cu and the C ABI in capi.cu).
+#pragma once
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/diffmpc.h"
+#include "ilqr_backward.cuh"
+
+namespace dmpc {
+
+int fail(const char* fmt, ...) __attribute__((format(printf, 1, 2)));
+extern std::atomic<int64_t> g_launches;
+int max_smem_optin();
+
+constexpr int group_size(int nx) { return nx <= 4 ? 4 : (nx <= 8 ? 8 : (nx <= 16 ? 16 : 32)); }
+
+
+template <class M>
+int check_theta(const DiffMPCProblem* p) {
+  if (p->n_theta != M::NTH) return fail("model kind %d expects %d parameters, got %d", M::KIND, M::NTH, p->n_theta);
+  return 0;
+}
+
+template <class Lay>
+int plan(int B, int T, int G, int& gpb, int& stride) {
+  const Lay L = Lay::make(T);
+  stride = L.total;
+  const int limit = max_smem_optin();
+  gpb = 128 / G;
+  while (gpb > 1 && gpb * stride > limit) gpb--;
+  if (gpb * stride > limit)
+    return fail("horizon T=%d needs %d bytes of shared memory per problem (limit %d)", T, stride, limit);
+  if (B < gpb) gpb = B > 0 ? B : 1;
+  return 0;
+}
+
+template <class M, bool DIAG, class R>
+int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s) {
+  constexpr int G = group_size(M::NX);
+  if (check_theta<M>(p)) return -1;
+  if (!io || !io->X || !io->U || !io->J || !io->C || !io->c || !io->x0 || !io->U_warm ||
+      (M::NTH > 0 && !io->theta))
+    return fail("forward: required pointer is NULL");
+  if (p->B == 0) return 0;
+  FwdArgs a;
+  memset(&a, 0, sizeof a);
+  a.B = p->B; a.T = p->T; a.K_max = p->K_max; a.n_alpha = p->n_alpha;
+  a.boxqp_max_iter = p->boxqp_max_iter; a.theta_stride = p->theta_stride;
+  a.dt = p->dt; a.conv_tol = p->conv_tol; a.boxqp_tol = p->boxqp_tol;
+  for (int i = 0; i < 8; i++) {
+    a.u_min[i] = p->u_min[i]; a.u_max[i] = p->u_max[i]; a.alphas[i] = p->alphas[i];
+  }
+  a.theta = io->theta; a.C = io->C; a.c = io->c; a.x0 = io->x0; a.U_warm = io->U_warm;
+  a.X = io->X; a.U = io->U; a.J = io->J; a.K = io->K; a.k = io->k; a.iters = io->iters;
+  a.converged = io->converged; a.diverged = io->diverged; a.fail_t = io->fail_t;
+  a.clamped = io->clamped; a.alpha_hist = io->alpha_hist; a.J_hist = io->J_hist;
+  if (plan<FwdLayout<M, DIAG, R>>(p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
+  const int smem = a.gpb * a.smem_stride;
+  auto kern = ilqr_forward_kernel<M, G, DIAG, R>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int blocks = (p->B + a.gpb - 1) / a.gpb;
+  kern<<<blocks, a.gpb * G, smem, s>>>(a);
+  g_launches.fetch_add(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail("forward launch failed: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+template <class M, bool DIAG, class R>
+int bwd_impl(const DiffMPCProblem* p, const DiffMPCBackwardIO* io, cudaStream_t s) {
+  constexpr int G = group_size(M::NX);
+  if (check_theta<M>(p)) return -1;
+  if (!io || !io->C || !io->X || !io->U || !io->dc || (M::NTH > 0 && !io->theta))
+    return fail("backward: required pointer is NULL");
+  if ((io->dtheta || io->dLdJ) && !io->c) return fail("backward: c is required for dtheta / dL/dJ");
+  if (p->B == 0) return 0;
+  BwdArgs a;
+  memset(&a, 0, sizeof a);
+  a.B = p->B; a.T = p->T; a.theta_stride = p->theta_stride; a.n_theta = p->n_theta; a.dt = p->dt;
+  for (int i = 0; i < 8; i++) {
+    a.u_min[i] = p->u_min[i]; a.u_max[i] = p->u_max[i];
+  }
+  a.theta = io->theta; a.C = io->C; a.c = io->c; a.X = io->X; a.U = io->U;
+  a.dLdX = io->dLdX; a.dLdU = io->dLdU; a.dLdJ = io->dLdJ;
+  a.dC = io->dC; a.dc = io->dc; a.dx0 = io->dx0; a.dtheta = io->dtheta; a.dX = io->dX; a.dU = io->dU;
+  a.fail_t = io->fail_t;
+  if (plan<BwdLayout<M, DIAG, R>>(p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
+  const int smem = a.gpb * a.smem_stride;
+  auto kern = ilqr_backward_kernel<M, G, DIAG, R>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int blocks = (p->B + a.gpb - 1) / a.gpb;
+  kern<<<blocks, a.gpb * G, smem, s>>>(a);
+  g_launches.fetch_add(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail("backward launch failed: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+// batched dynamics: one thread per point
+template <class M, class R>
+__global__ void dynamics_kernel(int N, int stride, double dt, const R* theta, const R* x, const R* u,
+                                R* xn, R* A, R* Bm) {
+  constexpr int NX = M::NX, NU = M::NU;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const R* th = theta + (size_t)stride * i;
+  R xr[NX], ur[NU];
+#pragma unroll
+  for (int a = 0; a < NX; a++) xr[a] = x[(size_t)i * NX + a];
+#pragma unroll
+  for (int a = 0; a < NU; a++) ur[a] = u[(size_t)i * NU + a];
+  R* Ai = A ? A + (size_t)i * NX * NX : nullptr;
+  R* Bi = Bm ? Bm + (size_t)i * NX * NU : nullptr;
+  if constexpr (M::kLinearParams) {
+    if (xn) {
+#pragma unroll
+      for (int a = 0; a < NX; a++) {
+        R acc = R(0);
+#pragma unroll
+        for (int b = 0; b < NX; b++) acc += th[a * NX + b] * xr[b];
+#pragma unroll
+        for (int b = 0; b < NU; b++) acc += th[NX * NX + a * NU + b] * ur[b];
+        xn[(size_t)i * NX + a] = acc;
+      }
+    }
+    if (Ai && Bi) {
+      for (int e = 0; e < NX * NX; e++) Ai[e] = th[e];
+      for (int e = 0; e < NX * NU; e++) Bi[e] = th[NX * NX + e];
+    }
+  } else {
+    constexpr int NTHL = M::NTH > 0 ? M::NTH : 1;
+    R thr[NTHL];
+#pragma unroll
+    for (int a = 0; a < NTHL; a++) thr[a] = a < M::NTH ? th[a] : R(0);
+    if (xn) {
+      R o[NX];
+      M::template step<R>(thr, (R)dt, xr, ur, o);
+#pragma unroll
+      for (int a = 0; a < NX; a++) xn[(size_t)i * NX + a] = o[a];
+    }
+    if (Ai && Bi) {
+      M::template jac_const<R>(thr, (R)dt, Ai, NX, Bi, 0, 1);
+      M::template jac_vary<R>(thr, (R)dt, xr, ur, Ai, NX, Bi);
+    }
+  }
+}
+
+template <class M, class R>
+int dyn_impl(const DiffMPCProblem* p, int N, const void* theta, const void* x, const void* u, void* xn,
+             void* A, void* Bm, cudaStream_t s) {
+  if (check_theta<M>(p)) return -1;
+  if (N <= 0) return 0;
+  if (!x || !u || (M::NTH > 0 && !theta)) return fail("dynamics: required pointer is NULL");
+  const int threads = 128, blocks = (N + threads - 1) / threads;
+  dynamics_kernel<M, R><<<blocks, threads, 0, s>>>(N, p->theta_stride, p->dt, (const R*)theta,
+                                                   (const R*)x, (const R*)u, (R*)xn, (R*)A, (R*)Bm);
+  g_launches.fetch_add(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail("dynamics launch failed: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+enum class Op { Fwd, Bwd, Dyn };
+
+struct Call {
+  Op op;
+  const DiffMPCProblem* p;
+  const DiffMPCForwardIO* fio;
+  const DiffMPCBackwardIO* bio;
+  int N;
+  const void *theta, *x, *u;
+  void *xn, *A, *Bm;
+  cudaStream_t s;
+};
+
+template <class M, class R>
+int run(const Call& c) {
+  const bool diag = c.p->cost_layout == DIFFMPC_COST_DIAG;
+  switch (c.op) {
+    case Op::Fwd:
+      return diag ? fwd_impl<M, true, R>(c.p, c.fio, c.s) : fwd_impl<M, false, R>(c.p, c.fio, c.s);
+    case Op::Bwd:
+      return diag ? bwd_impl<M, true, R>(c.p, c.bio, c.s) : bwd_impl<M, false, R>(c.p, c.bio, c.s);
+    default:
+      return dyn_impl<M, R>(c.p, c.N, c.theta, c.x, c.u, c.xn, c.A, c.Bm, c.s);
+  }
+}
+
+}  // namespace dmpc

@@ -1,0 +1,286 @@
+// models.cuh — dynamics models for the B200 DiffMPC kernels.
+//
+// Each model is a stateless trait with compile-time dimensions and templated
+// device functions, so the same model code runs in float (Riccati / backward,
+// f32 mode) and double (trajectory rollouts and cost evaluation).
+//
+//   step(th, dt, x, u, out)            x+ = f(x,u)           (kernels.py:43-73)
+//   jac_const(th, dt, A, lda, B, l, G) every entry of A = df/dx, B = df/du that
+//                                      does not depend on (x,u) (zeros, ones, dt
+//                                      terms, constant mixer rows) — written once
+//                                      per kernel, cooperatively by the G lanes
+//   jac_vary(th, dt, x, u, A, lda, B)  the state-dependent entries only, rewritten
+//                                      every stage (kernels.py:76-117)
+//   theta_grad(...)                    dL/dtheta contributions of one stage
+//                                      (SURVEY.md §8(a) NEW row)
+//
+// `th` points to the model parameters: a small register array for the quadrotors,
+// the smem copy of [A,B] for the linear model. Expression trees of the planar and
+// 13-state quadrotor steps follow oracle/diffmpc_oracle.c token for token.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace dmpc {
+
+#define DMPC_DEV __device__ __forceinline__
+
+constexpr double kInvSqrt2 = 0.7071067811865476;
+
+// ---------------------------------------------------------------------------
+// double integrator, d = NU (kernels.py:47-51, 85-91)
+// ---------------------------------------------------------------------------
+template <int D>
+struct DoubleIntegrator {
+  static constexpr int NX = 2 * D, NU = D, NTH = 0, KIND = 0;
+  static constexpr bool kLinearParams = false;
+  template <class S>
+  DMPC_DEV static void step(const S*, S dt, const S* x, const S* u, S* o) {
+#pragma unroll
+    for (int i = 0; i < D; i++) {
+      o[i] = x[i] + dt * x[D + i];
+      o[D + i] = x[D + i] + dt * u[i];
+    }
+  }
+  template <class S>
+  DMPC_DEV static void jac_const(const S*, S dt, S* A, int lda, S* B, int lane, int G) {
+    for (int e = lane; e < NX * NX; e += G) {
+      int i = e / NX, j = e % NX;
+      A[i * lda + j] = (i == j) ? S(1) : ((i < D && j == i + D) ? dt : S(0));
+    }
+    for (int e = lane; e < NX * NU; e += G) {
+      int i = e / NU, j = e % NU;
+      B[i * NU + j] = (i >= D && i - D == j) ? dt : S(0);
+    }
+  }
+  template <class S>
+  DMPC_DEV static void jac_vary(const S*, S, const S*, const S*, S*, int, S*) {}
+  template <class S>
+  DMPC_DEV static void theta_grad(const S*, S, const S*, const S*, const S*, const S*, const S*,
+                                  const S*, S*) {}
+};
+
+// ---------------------------------------------------------------------------
+// planar quadrotor, x = [px, py, theta, vx, vy, omega], u = [u_left, u_right],
+// th = [m, arm, I, g] (dynamics.py:57-70, kernels.py:52-65, 92-111)
+// ---------------------------------------------------------------------------
+struct PlanarQuad {
+  static constexpr int NX = 6, NU = 2, NTH = 4, KIND = 1;
+  static constexpr bool kLinearParams = false;
+  template <class S>
+  DMPC_DEV static void step(const S* th, S dt, const S* x, const S* u, S* o) {
+    const S m = th[0], arm = th[1], inertia = th[2], g = th[3];
+    S s, c;
+    sincos_(x[2], &s, &c);
+    const S thrust = u[0] + u[1];
+    o[0] = x[0] + dt * x[3];
+    o[1] = x[1] + dt * x[4];
+    o[2] = x[2] + dt * x[5];
+    o[3] = x[3] + dt * (-thrust * s / m);
+    o[4] = x[4] + dt * (thrust * c / m - g);
+    o[5] = x[5] + dt * (arm * (u[1] - u[0]) / inertia);
+  }
+  template <class S>
+  DMPC_DEV static void jac_const(const S* th, S dt, S* A, int lda, S* B, int lane, int G) {
+    for (int e = lane; e < NX * NX; e += G) {
+      int i = e / NX, j = e % NX;
+      A[i * lda + j] = (i == j) ? S(1) : ((i < 3 && j == i + 3) ? dt : S(0));
+    }
+    for (int e = lane; e < NX * NU; e += G) B[e] = S(0);
+    if (lane == 0) {
+      B[5 * 2 + 0] = -dt * th[1] / th[2];
+      B[5 * 2 + 1] = dt * th[1] / th[2];
+    }
+  }
+  template <class S>
+  DMPC_DEV static void jac_vary(const S* th, S dt, const S* x, const S* u, S* A, int lda, S* B) {
+    const S m = th[0];
+    S s, c;
+    sincos_(x[2], &s, &c);
+    const S thrust = u[0] + u[1];
+    A[3 * lda + 2] = -dt * thrust * c / m;
+    A[4 * lda + 2] = -dt * thrust * s / m;
+    B[3 * 2 + 0] = -dt * s / m;
+    B[3 * 2 + 1] = -dt * s / m;
+    B[4 * 2 + 0] = dt * c / m;
+    B[4 * 2 + 1] = dt * c / m;
+  }
+  // g[p] += lh . df/dth_p + lam . (d2f/dth_p dz) dz   (oracle: theta_grad_stage)
+  template <class S>
+  DMPC_DEV static void theta_grad(const S* th, S dt, const S* x, const S* u, const S* dx,
+                                  const S* du, const S* lh, const S* lam, S* g) {
+    const S m = th[0], arm = th[1], I = th[2];
+    S s, c;
+    sincos_(x[2], &s, &c);
+    const S F = u[0] + u[1], dF = du[0] + du[1], dd = u[1] - u[0], ddd = du[1] - du[0];
+    const S mm = m * m;
+    g[0] += lh[3] * (dt * F * s / mm) + lh[4] * (-dt * F * c / mm) +
+            lam[3] * (dt * (F * c * dx[2] + s * dF) / mm) +
+            lam[4] * (dt * (F * s * dx[2] - c * dF) / mm);
+    g[1] += lh[5] * (dt * dd / I) + lam[5] * (dt * ddd / I);
+    g[2] += lh[5] * (-dt * arm * dd / (I * I)) + lam[5] * (-dt * arm * ddd / (I * I));
+    g[3] += lh[4] * (-dt);
+  }
+
+ private:
+  DMPC_DEV static void sincos_(double a, double* s, double* c) { sincos(a, s, c); }
+  DMPC_DEV static void sincos_(float a, float* s, float* c) { sincosf(a, s, c); }
+};
+
+// ---------------------------------------------------------------------------
+// 13-state quadrotor (kind 3). x = [p(3), q(4: w,x,y,z), v(3), w(3)], u = 4 rotors,
+// th = [m, arm, Jx, Jy, Jz, kappa, g]. See paper_2605_29155_b200/dynamics.py.
+// ---------------------------------------------------------------------------
+struct Quad13 {
+  static constexpr int NX = 13, NU = 4, NTH = 7, KIND = 3;
+  static constexpr bool kLinearParams = false;
+  template <class S>
+  DMPC_DEV static void step(const S* th, S dt, const S* x, const S* u, S* o) {
+    const S m = th[0], l = th[1], Jx = th[2], Jy = th[3], Jz = th[4], kap = th[5], g = th[6];
+    const S d = l * S(kInvSqrt2);
+    const S qw = x[3], qx = x[4], qy = x[5], qz = x[6];
+    const S wx = x[10], wy = x[11], wz = x[12];
+    const S F = ((u[0] + u[1]) + u[2]) + u[3];
+    const S tx = d * (((u[0] + u[1]) - u[2]) - u[3]);
+    const S ty = d * (((u[1] - u[0]) + u[2]) - u[3]);
+    const S tz = kap * (((u[0] - u[1]) + u[2]) - u[3]);
+    const S hw = S(0.5) * dt;
+    const S r13 = S(2) * (qx * qz + qw * qy);
+    const S r23 = S(2) * (qy * qz - qw * qx);
+    const S r33 = S(1) - S(2) * (qx * qx + qy * qy);
+    const S a = F / m;
+    o[0] = x[0] + dt * x[7];
+    o[1] = x[1] + dt * x[8];
+    o[2] = x[2] + dt * x[9];
+    o[3] = qw + hw * (((-qx * wx) - qy * wy) - qz * wz);
+    o[4] = qx + hw * ((qw * wx + qy * wz) - qz * wy);
+    o[5] = qy + hw * ((qw * wy - qx * wz) + qz * wx);
+    o[6] = qz + hw * ((qw * wz + qx * wy) - qy * wx);
+    o[7] = x[7] + dt * (r13 * a);
+    o[8] = x[8] + dt * (r23 * a);
+    o[9] = x[9] + dt * (r33 * a - g);
+    o[10] = wx + dt * ((tx - (Jz - Jy) * wy * wz) / Jx);
+    o[11] = wy + dt * ((ty - (Jx - Jz) * wz * wx) / Jy);
+    o[12] = wz + dt * ((tz - (Jy - Jx) * wx * wy) / Jz);
+  }
+  template <class S>
+  DMPC_DEV static void jac_const(const S* th, S dt, S* A, int lda, S* B, int lane, int G) {
+    for (int e = lane; e < NX * NX; e += G) {
+      int i = e / NX, j = e % NX;
+      A[i * lda + j] = (i == j) ? S(1) : ((i < 3 && j == i + 7) ? dt : S(0));
+    }
+    for (int e = lane; e < NX * NU; e += G) B[e] = S(0);
+    if (lane == 0) {
+      const S d = th[1] * S(kInvSqrt2);
+      const S bx = dt * d / th[2], by = dt * d / th[3], bz = dt * th[5] / th[4];
+      B[10 * 4 + 0] = bx;  B[10 * 4 + 1] = bx;  B[10 * 4 + 2] = -bx; B[10 * 4 + 3] = -bx;
+      B[11 * 4 + 0] = -by; B[11 * 4 + 1] = by;  B[11 * 4 + 2] = by;  B[11 * 4 + 3] = -by;
+      B[12 * 4 + 0] = bz;  B[12 * 4 + 1] = -bz; B[12 * 4 + 2] = bz;  B[12 * 4 + 3] = -bz;
+    }
+  }
+  template <class S>
+  DMPC_DEV static void jac_vary(const S* th, S dt, const S* x, const S* u, S* A, int lda, S* B) {
+    const S m = th[0], Jx = th[2], Jy = th[3], Jz = th[4];
+    const S qw = x[3], qx = x[4], qy = x[5], qz = x[6];
+    const S wx = x[10], wy = x[11], wz = x[12];
+    const S F = ((u[0] + u[1]) + u[2]) + u[3];
+    const S hw = S(0.5) * dt;
+    const S a = F / m;
+    const S r13 = S(2) * (qx * qz + qw * qy);
+    const S r23 = S(2) * (qy * qz - qw * qx);
+    const S r33 = S(1) - S(2) * (qx * qx + qy * qy);
+    A[3 * lda + 4] = -hw * wx; A[3 * lda + 5] = -hw * wy; A[3 * lda + 6] = -hw * wz;
+    A[3 * lda + 10] = -hw * qx; A[3 * lda + 11] = -hw * qy; A[3 * lda + 12] = -hw * qz;
+    A[4 * lda + 3] = hw * wx; A[4 * lda + 5] = hw * wz; A[4 * lda + 6] = -hw * wy;
+    A[4 * lda + 10] = hw * qw; A[4 * lda + 11] = -hw * qz; A[4 * lda + 12] = hw * qy;
+    A[5 * lda + 3] = hw * wy; A[5 * lda + 4] = -hw * wz; A[5 * lda + 6] = hw * wx;
+    A[5 * lda + 10] = hw * qz; A[5 * lda + 11] = hw * qw; A[5 * lda + 12] = -hw * qx;
+    A[6 * lda + 3] = hw * wz; A[6 * lda + 4] = hw * wy; A[6 * lda + 5] = -hw * wx;
+    A[6 * lda + 10] = -hw * qy; A[6 * lda + 11] = hw * qx; A[6 * lda + 12] = hw * qw;
+    const S da = dt * a;
+    A[7 * lda + 3] = da * (S(2) * qy); A[7 * lda + 4] = da * (S(2) * qz);
+    A[7 * lda + 5] = da * (S(2) * qw); A[7 * lda + 6] = da * (S(2) * qx);
+    A[8 * lda + 3] = da * (S(-2) * qx); A[8 * lda + 4] = da * (S(-2) * qw);
+    A[8 * lda + 5] = da * (S(2) * qz); A[8 * lda + 6] = da * (S(2) * qy);
+    A[9 * lda + 4] = da * (S(-4) * qx); A[9 * lda + 5] = da * (S(-4) * qy);
+    const S b7 = dt * r13 / m, b8 = dt * r23 / m, b9 = dt * r33 / m;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      B[7 * 4 + j] = b7;
+      B[8 * 4 + j] = b8;
+      B[9 * 4 + j] = b9;
+    }
+    A[10 * lda + 11] = -dt * ((Jz - Jy) * wz) / Jx; A[10 * lda + 12] = -dt * ((Jz - Jy) * wy) / Jx;
+    A[11 * lda + 10] = -dt * ((Jx - Jz) * wz) / Jy; A[11 * lda + 12] = -dt * ((Jx - Jz) * wx) / Jy;
+    A[12 * lda + 10] = -dt * ((Jy - Jx) * wy) / Jz; A[12 * lda + 11] = -dt * ((Jy - Jx) * wx) / Jz;
+  }
+  template <class S>
+  DMPC_DEV static void theta_grad(const S* th, S dt, const S* x, const S* u, const S* dx,
+                                  const S* du, const S* lh, const S* lam, S* g) {
+    const S m = th[0], l = th[1], Jx = th[2], Jy = th[3], Jz = th[4], kap = th[5];
+    const S d = l * S(kInvSqrt2);
+    const S qw = x[3], qx = x[4], qy = x[5], qz = x[6];
+    const S wx = x[10], wy = x[11], wz = x[12];
+    const S dqw = dx[3], dqx = dx[4], dqy = dx[5], dqz = dx[6];
+    const S dwx = dx[10], dwy = dx[11], dwz = dx[12];
+    const S F = ((u[0] + u[1]) + u[2]) + u[3];
+    const S dF = ((du[0] + du[1]) + du[2]) + du[3];
+    const S sx = ((u[0] + u[1]) - u[2]) - u[3], dsx = ((du[0] + du[1]) - du[2]) - du[3];
+    const S sy = ((u[1] - u[0]) + u[2]) - u[3], dsy = ((du[1] - du[0]) + du[2]) - du[3];
+    const S sz = ((u[0] - u[1]) + u[2]) - u[3], dsz = ((du[0] - du[1]) + du[2]) - du[3];
+    const S tx = d * sx, ty = d * sy, tz = kap * sz;
+    const S r13 = S(2) * (qx * qz + qw * qy), r23 = S(2) * (qy * qz - qw * qx);
+    const S r33 = S(1) - S(2) * (qx * qx + qy * qy);
+    const S dr13 = S(2) * (qy * dqw + qz * dqx + qw * dqy + qx * dqz);
+    const S dr23 = S(2) * (-qx * dqw - qw * dqx + qz * dqy + qy * dqz);
+    const S dr33 = S(-4) * (qx * dqx + qy * dqy);
+    const S im2 = dt / (m * m);
+    g[0] += -im2 * F * (lh[7] * r13 + lh[8] * r23 + lh[9] * r33) -
+            im2 * (lam[7] * (F * dr13 + r13 * dF) + lam[8] * (F * dr23 + r23 * dF) +
+                   lam[9] * (F * dr33 + r33 * dF));
+    const S c = S(kInvSqrt2);
+    g[1] += lh[10] * (dt * c * sx / Jx) + lh[11] * (dt * c * sy / Jy) +
+            lam[10] * (dt * c * dsx / Jx) + lam[11] * (dt * c * dsy / Jy);
+    const S e10 = tx - (Jz - Jy) * wy * wz, e11 = ty - (Jx - Jz) * wz * wx,
+            e12 = tz - (Jy - Jx) * wx * wy;
+    const S de10 = d * dsx - (Jz - Jy) * (wz * dwy + wy * dwz);
+    const S de11 = d * dsy - (Jx - Jz) * (wx * dwz + wz * dwx);
+    const S de12 = kap * dsz - (Jy - Jx) * (wy * dwx + wx * dwy);
+    const S pyz = wy * wz, pzx = wz * wx, pxy = wx * wy;
+    const S dpyz = wz * dwy + wy * dwz, dpzx = wx * dwz + wz * dwx, dpxy = wy * dwx + wx * dwy;
+    g[2] += lh[10] * (-dt * e10 / (Jx * Jx)) + lh[11] * (-dt * pzx / Jy) + lh[12] * (dt * pxy / Jz) +
+            lam[10] * (-dt * de10 / (Jx * Jx)) + lam[11] * (-dt * dpzx / Jy) +
+            lam[12] * (dt * dpxy / Jz);
+    g[3] += lh[10] * (dt * pyz / Jx) + lh[11] * (-dt * e11 / (Jy * Jy)) + lh[12] * (-dt * pxy / Jz) +
+            lam[10] * (dt * dpyz / Jx) + lam[11] * (-dt * de11 / (Jy * Jy)) +
+            lam[12] * (-dt * dpxy / Jz);
+    g[4] += lh[10] * (-dt * pyz / Jx) + lh[11] * (dt * pzx / Jy) + lh[12] * (-dt * e12 / (Jz * Jz)) +
+            lam[10] * (-dt * dpyz / Jx) + lam[11] * (dt * dpzx / Jy) +
+            lam[12] * (-dt * de12 / (Jz * Jz));
+    g[5] += lh[12] * (dt * sz / Jz) + lam[12] * (dt * dsz / Jz);
+    g[6] += lh[9] * (-dt);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// linear model x+ = A x + B u, th = [A row-major, B row-major] (kernels.py:66-73, 112-117).
+// The kernels keep [A | B] in shared memory (jac_const copies th there once); `step`
+// reads from that copy, so `th` passed to step/jac_vary is the smem A (lda) / B pair.
+// ---------------------------------------------------------------------------
+template <int NX_, int NU_>
+struct LinearModel {
+  static constexpr int NX = NX_, NU = NU_, NTH = NX_ * NX_ + NX_ * NU_, KIND = 2;
+  static constexpr bool kLinearParams = true;
+};
+
+}  // namespace dmpc
+
+namespace dmpc {
+using DoubleIntegrator1 = DoubleIntegrator<1>;
+using DoubleIntegrator2 = DoubleIntegrator<2>;
+using DoubleIntegrator3 = DoubleIntegrator<3>;
+using Linear1x1 = LinearModel<1, 1>;
+using Linear2x1 = LinearModel<2, 1>;
+using Linear3x2 = LinearModel<3, 2>;
+using Linear4x2 = LinearModel<4, 2>;
+using Linear13x4 = LinearModel<13, 4>;
+}  // namespace dmpc
