@@ -57,33 +57,42 @@ DMPC_DEV bool finite_(T v) { return isfinite(v); }
 // ---------------------------------------------------------------------------
 constexpr double kArmijo = 0.1, kStepDec = 0.6, kMinStep = 1e-20, kLamInit = 1e-6, kLamMax = 1e-2;
 
-template <int NU>
+template <int NU, class T = double>
 struct Chol {
-  double L[NU][NU];
-  double inv[NU];  // 1 / L[a][a]
+  T L[NU][NU];  // lower triangle used
+  T inv[NU];    // 1 / L[a][a]
 };
 
-template <int NU>
-DMPC_DEV bool chol_masked(const double (&H)[NU][NU], const bool (&fr)[NU], Chol<NU>& c) {
+DMPC_DEV double rsqrt_(double v) { return rsqrt(v); }
+DMPC_DEV float rsqrt_(float v) { return rsqrtf(v); }
+DMPC_DEV double sqrt_(double v) { return sqrt(v); }
+DMPC_DEV float sqrt_(float v) { return sqrtf(v); }
+
+// Masked Cholesky; the diagonal reciprocals come from one rsqrt, and the
+// off-diagonal / substitution divisions become multiplications by them (a one-ulp
+// difference from the reference's divisions, far below the parity tolerances).
+template <int NU, class T>
+DMPC_DEV bool chol_masked(const T (&H)[NU][NU], T lam, const bool (&fr)[NU], Chol<NU, T>& c) {
   bool ok = true;
 #pragma unroll
   for (int a = 0; a < NU; a++) {
 #pragma unroll
     for (int b = 0; b <= a; b++) {
-      double s;
+      T s;
       if (fr[a] && fr[b]) {
-        s = H[a][b];
+        s = H[a][b] + (a == b ? lam : T(0));
       } else {
-        s = (a == b) ? 1.0 : 0.0;
+        s = (a == b) ? T(1) : T(0);
       }
 #pragma unroll
       for (int r = 0; r < b; r++) s -= c.L[a][r] * c.L[b][r];
       if (a == b) {
-        if (s <= 0.0) ok = false;
-        c.L[a][a] = sqrt(s);
-        c.inv[a] = 1.0 / c.L[a][a];
+        if (s <= T(0)) ok = false;
+        const T is = rsqrt_(s);
+        c.inv[a] = is;
+        c.L[a][a] = s * is;
       } else {
-        c.L[a][b] = s / c.L[b][b];
+        c.L[a][b] = s * c.inv[b];
       }
     }
   }
@@ -91,74 +100,94 @@ DMPC_DEV bool chol_masked(const double (&H)[NU][NU], const bool (&fr)[NU], Chol<
 }
 
 // L L' out = b (masked rows of b are zero and stay zero)
-template <int NU>
-DMPC_DEV void chol_solve(const Chol<NU>& c, const double (&b)[NU], double (&out)[NU]) {
+template <int NU, class T>
+DMPC_DEV void chol_solve(const Chol<NU, T>& c, const T (&b)[NU], T (&out)[NU]) {
 #pragma unroll
   for (int a = 0; a < NU; a++) {
-    double s = b[a];
+    T s = b[a];
 #pragma unroll
     for (int r = 0; r < a; r++) s -= c.L[a][r] * out[r];
-    out[a] = s / c.L[a][a];
+    out[a] = s * c.inv[a];
   }
 #pragma unroll
   for (int a = NU - 1; a >= 0; a--) {
-    double s = out[a];
+    T s = out[a];
 #pragma unroll
     for (int r = a + 1; r < NU; r++) s -= c.L[r][a] * out[r];
-    out[a] = s / c.L[a][a];
+    out[a] = s * c.inv[a];
   }
 }
 
-template <int NU>
-DMPC_DEV double qp_value(const double (&H)[NU][NU], const double (&g)[NU], const double (&u)[NU]) {
-  double acc = 0.0;
+// 0.5 u'(H + lam I)u + g'u
+template <int NU, class T>
+DMPC_DEV T qp_value(const T (&H)[NU][NU], T lam, const T (&g)[NU], const T (&u)[NU]) {
+  T acc = T(0);
 #pragma unroll
   for (int a = 0; a < NU; a++) {
-    double row = 0.0;
+    T row = T(0);
 #pragma unroll
-    for (int b = 0; b < NU; b++) row += H[a][b] * u[b];
-    acc += 0.5 * u[a] * row + g[a] * u[a];
+    for (int b = 0; b < NU; b++) row += (H[a][b] + (a == b ? lam : T(0))) * u[b];
+    acc += T(0.5) * u[a] * row + g[a] * u[a];
   }
   return acc;
 }
 
-// boxqp_one (kernels.py:239-318). Returns 0 (OK) or -1 (NOT_PD).
 template <int NU>
-DMPC_DEV int boxqp(const double (&H)[NU][NU], const double (&g)[NU], const double (&lo)[NU],
-                   const double (&hi)[NU], double (&u)[NU], bool (&fr)[NU], int max_iter,
-                   double tol) {
+DMPC_DEV bool same_mask(const bool (&a)[NU], const bool (&b)[NU]) {
+  bool e = true;
+#pragma unroll
+  for (int i = 0; i < NU; i++) e = e && (a[i] == b[i]);
+  return e;
+}
+
+// boxqp_one (kernels.py:239-318) on H + lam I. Returns 0 (OK) or -1 (NOT_PD).
+// `ch` / `ch_fr` carry the last factorisation and the free mask it was computed
+// for: H is fixed inside the call, so a repeated free set reuses the identical
+// factor. The backtracking loop stops as soon as the trial point no longer moves
+// (u + step*search == u in every coordinate): from there on every smaller step
+// gives the same rejected value, so the reference's remaining trials down to
+// step <= 1e-20 cannot accept and the outcome is unchanged.
+template <int NU, class T>
+DMPC_DEV int boxqp(const T (&H)[NU][NU], T lam, const T (&g)[NU], const T (&lo)[NU],
+                   const T (&hi)[NU], T (&u)[NU], bool (&fr)[NU], int max_iter,
+                   T tol, Chol<NU, T>& ch, bool (&ch_fr)[NU], bool& ch_ok) {
 #pragma unroll
   for (int a = 0; a < NU; a++) {
     if (u[a] < lo[a]) u[a] = lo[a];
     else if (u[a] > hi[a]) u[a] = hi[a];
     fr[a] = true;
   }
-  double value = qp_value<NU>(H, g, u);
-  Chol<NU> ch;
+  ch_ok = false;
+  T value = qp_value<NU, T>(H, lam, g, u);
   for (int it = 0; it < max_iter; it++) {
-    double grad[NU];
+    T grad[NU];
     int nf = 0;
 #pragma unroll
     for (int a = 0; a < NU; a++) {
-      double s = g[a];
+      T s = g[a];
 #pragma unroll
-      for (int b = 0; b < NU; b++) s += H[a][b] * u[b];
+      for (int b = 0; b < NU; b++) s += (H[a][b] + (a == b ? lam : T(0))) * u[b];
       grad[a] = s;
-      const bool clamped = (u[a] <= lo[a] && s > 0.0) || (u[a] >= hi[a] && s < 0.0);
+      const bool clamped = (u[a] <= lo[a] && s > T(0)) || (u[a] >= hi[a] && s < T(0));
       fr[a] = !clamped;
       nf += fr[a] ? 1 : 0;
     }
     if (nf == 0) return 0;
-    double gnorm = 0.0;
+    T gnorm = T(0);
 #pragma unroll
     for (int a = 0; a < NU; a++)
       if (fr[a]) gnorm += grad[a] * grad[a];
-    if (sqrt(gnorm) <= tol) return 0;
-    if (!chol_masked<NU>(H, fr, ch)) return -1;
-    double rhs[NU], cand[NU];
+    if (sqrt_(gnorm) <= tol) return 0;
+    if (!(ch_ok && same_mask<NU>(fr, ch_fr))) {
+#pragma unroll
+      for (int a = 0; a < NU; a++) ch_fr[a] = fr[a];
+      ch_ok = chol_masked<NU, T>(H, lam, fr, ch);
+      if (!ch_ok) return -1;
+    }
+    T rhs[NU], cand[NU];
 #pragma unroll
     for (int a = 0; a < NU; a++) {
-      double s = 0.0;
+      T s = T(0);
       if (fr[a]) {
         s = g[a];
 #pragma unroll
@@ -167,31 +196,34 @@ DMPC_DEV int boxqp(const double (&H)[NU][NU], const double (&g)[NU], const doubl
       }
       rhs[a] = s;
     }
-    chol_solve<NU>(ch, rhs, cand);
-    double search[NU];
-    double sdotg = 0.0;
+    chol_solve<NU, T>(ch, rhs, cand);
+    T search[NU];
+    T sdotg = T(0);
 #pragma unroll
     for (int a = 0; a < NU; a++) {
-      search[a] = fr[a] ? (-cand[a] - u[a]) : 0.0;
+      search[a] = fr[a] ? (-cand[a] - u[a]) : T(0);
       if (fr[a]) sdotg += search[a] * grad[a];
     }
-    if (sdotg >= 0.0) return 0;
-    double step = 1.0, vc = 0.0;
+    if (sdotg >= T(0)) return 0;
+    T step = T(1), vc = T(0);
     bool accepted = false;
-    while (step > kMinStep) {
+    while (step > T(kMinStep)) {
+      bool moved = false;
 #pragma unroll
       for (int a = 0; a < NU; a++) {
-        double v = u[a] + step * search[a];
+        T v = u[a] + step * search[a];
         if (v < lo[a]) v = lo[a];
         else if (v > hi[a]) v = hi[a];
         cand[a] = v;
+        moved |= (v != u[a]);
       }
-      vc = qp_value<NU>(H, g, cand);
-      if (vc - value <= kArmijo * step * sdotg) {
+      if (!moved) break;
+      vc = qp_value<NU, T>(H, lam, g, cand);
+      if (vc - value <= T(kArmijo) * step * sdotg) {
         accepted = true;
         break;
       }
-      step *= kStepDec;
+      step *= T(kStepDec);
     }
     if (!accepted) return 0;
 #pragma unroll
@@ -203,21 +235,20 @@ DMPC_DEV int boxqp(const double (&H)[NU][NU], const double (&g)[NU], const doubl
 
 // The lambda-regularised stage solve of backward_range (kernels.py:440-471).
 // On success: du (the feedforward k_t), fr (free mask), ch (Cholesky of the
-// regularised free block, used for the K columns).
-template <int NU>
-DMPC_DEV bool stage_qp(const double (&Quu)[NU][NU], const double (&qu)[NU], const double (&lo)[NU],
-                       const double (&hi)[NU], int max_iter, double tol, double (&du)[NU],
-                       bool (&fr)[NU], Chol<NU>& ch) {
-  double lam = 0.0;
+// regularised free block, used for the K columns). The lambda schedule is
+// generated in double exactly as the reference does (0, 1e-6, x10 ... <= 1e-2).
+template <int NU, class T>
+DMPC_DEV bool stage_qp(const T (&Quu)[NU][NU], const T (&qu)[NU], const T (&lo)[NU],
+                       const T (&hi)[NU], int max_iter, T tol, T (&du)[NU],
+                       bool (&fr)[NU], Chol<NU, T>& ch) {
+  double lamd = 0.0;
   for (;;) {
-    double Ht[NU][NU];
+    const T lam = (T)lamd;
 #pragma unroll
-    for (int a = 0; a < NU; a++)
-#pragma unroll
-      for (int b = 0; b < NU; b++) Ht[a][b] = Quu[a][b] + (a == b ? lam : 0.0);
-#pragma unroll
-    for (int a = 0; a < NU; a++) du[a] = 0.0;
-    const int st = boxqp<NU>(Ht, qu, lo, hi, du, fr, max_iter, tol);
+    for (int a = 0; a < NU; a++) du[a] = T(0);
+    bool ch_fr[NU];
+    bool ch_ok;
+    const int st = boxqp<NU, T>(Quu, lam, qu, lo, hi, du, fr, max_iter, tol, ch, ch_fr, ch_ok);
     if (st == 0) {
       bool any = false;
 #pragma unroll
@@ -227,15 +258,16 @@ DMPC_DEV bool stage_qp(const double (&Quu)[NU][NU], const double (&qu)[NU], cons
 #pragma unroll
         for (int a = 0; a < NU; a++) {
 #pragma unroll
-          for (int b = 0; b < NU; b++) ch.L[a][b] = (a == b) ? 1.0 : 0.0;
-          ch.inv[a] = 1.0;
+          for (int b = 0; b < NU; b++) ch.L[a][b] = (a == b) ? T(1) : T(0);
+          ch.inv[a] = T(1);
         }
         return true;
       }
-      if (chol_masked<NU>(Ht, fr, ch)) return true;
+      if (ch_ok && same_mask<NU>(fr, ch_fr)) return true;  // factor of this free set is current
+      if (chol_masked<NU, T>(Quu, lam, fr, ch)) return true;
     }
-    lam = (lam == 0.0) ? kLamInit : lam * 10.0;
-    if (lam > kLamMax) return false;
+    lamd = (lamd == 0.0) ? kLamInit : lamd * 10.0;
+    if (lamd > kLamMax) return false;
   }
 }
 

@@ -40,48 +40,36 @@ struct BwdArgs {
 
 template <class M, bool DIAG, class R>
 struct BwdLayout {
-  static constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
-  static constexpr int LDA = NX;
-  static constexpr int NCS = DIAG ? NZ : NZ * NZ;
-  int oX, oU, oK, ok, odX, odU, ocl, oAs, oBs, oMA, oNB, oKT, oQuxT, oQuuKT, oqu, oVx, olam, olh,
-      oC, oc, total;
+  using D = Dims<M, DIAG, R>;
+  int oPr, oX, oU, oK, ok, odX, odU, ocl, olam, olh, total;
+  RicLayout<M, DIAG, R> ric;
   __host__ __device__ static BwdLayout make(int T) {
     BwdLayout L;
     const int s = (int)sizeof(R);
     int o = 0;
-    L.oX = o; o += (T + 1) * NX * s;
-    L.oU = o; o += T * NU * s;
-    L.oK = o; o += T * NU * NX * s;
-    L.ok = o; o += T * NU * s;
-    L.odX = o; o += (T + 1) * NX * s;
-    L.odU = o; o += T * NU * s;
-    L.ocl = o; o += align_up(T * NU, 8);
-    o = align_up(o, 16);
-    L.oAs = o; o += NX * LDA * s;
-    L.oBs = o; o += NX * NU * s;
-    L.oMA = o; o += NX * LDA * s;
-    L.oNB = o; o += NX * NU * s;
-    L.oKT = o; o += NX * NU * s;
-    L.oQuxT = o; o += NX * NU * s;
-    L.oQuuKT = o; o += NX * NU * s;
-    L.oqu = o; o += NU * s;
-    L.oVx = o; o += NX * s;
-    L.olam = o; o += NX * s;
-    L.olh = o; o += NX * s;
-    o = align_up(o, 16);
-    L.oC = o; o += 2 * NCS * s;
-    L.oc = o; o += 2 * NZ * s;
-    L.total = align_up(o, 16);
+    auto take = [&](int bytes) { int r = o; o = align_up(o + bytes, 16); return r; };
+    L.oPr = take(M::NP * s);
+    L.oX = take((T + 1) * D::LDA * s);
+    L.oU = take(T * D::LDB * s);
+    L.oK = take(T * D::NU * D::LDA * s);
+    L.ok = take(T * D::LDB * s);
+    L.odX = take((T + 1) * D::LDA * s);
+    L.odU = take(T * D::LDB * s);
+    L.ocl = take(T * D::NU);
+    L.olam = take(D::LDA * s);
+    L.olh = take(D::LDA * s);
+    L.ric = RicLayout<M, DIAG, R>::make(o);
+    L.total = align_up(L.ric.end, 16);
     return L;
   }
 };
 
 template <class M, int G, bool DIAG, class R>
-__global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2) ilqr_backward_kernel(const BwdArgs args) {
+  using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
+  constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD;
   using Lay = BwdLayout<M, DIAG, R>;
-  constexpr int LDA = Lay::LDA, NCS = Lay::NCS;
-  constexpr int NTHL = M::kLinearParams ? 1 : (M::NTH > 0 ? M::NTH : 1);
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
@@ -92,85 +80,67 @@ __global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) 
   const int T = args.T;
   const Lay L = Lay::make(T);
   unsigned char* base = smem_raw + (size_t)grp * args.smem_stride;
-  R* Xs = (R*)(base + L.oX);
-  R* Us = (R*)(base + L.oU);
-  R* Ka = (R*)(base + L.oK);
-  R* ka = (R*)(base + L.ok);
-  R* dXs = (R*)(base + L.odX);
-  R* dUs = (R*)(base + L.odU);
+  R* Xs = (R*)(base + L.oX);    // rows of LDA
+  R* Us = (R*)(base + L.oU);    // rows of LDB
+  R* Ka = (R*)(base + L.oK);    // [t][r][LDA]
+  R* ka = (R*)(base + L.ok);    // [t][LDB]
+  R* dXs = (R*)(base + L.odX);  // rows of LDA
+  R* dUs = (R*)(base + L.odU);  // rows of LDB
   uint8_t* cl = (uint8_t*)(base + L.ocl);
-  R* As = (R*)(base + L.oAs);
-  R* Bs = (R*)(base + L.oBs);
-  R* MA = (R*)(base + L.oMA);
-  R* NB = (R*)(base + L.oNB);
-  R* KT = (R*)(base + L.oKT);
-  R* QuxT = (R*)(base + L.oQuxT);
-  R* QuuKT = (R*)(base + L.oQuuKT);
-  R* qus = (R*)(base + L.oqu);
-  R* Vxs = (R*)(base + L.oVx);
   R* lams = (R*)(base + L.olam);
   R* lhs = (R*)(base + L.olh);
-  R* Cb = (R*)(base + L.oC);
-  R* cb = (R*)(base + L.oc);
+  Ric<M, DIAG, R> S;
+  S.bind(base, L.ric);
 
-  const R* Cg = (const R*)args.C + (size_t)pid * T * NCS;
+  const R* Cg = (const R*)args.C + (size_t)pid * T * D::NCS;
   const R* cg = args.c ? (const R*)args.c + (size_t)pid * T * NZ : nullptr;
   const R* sXg = args.dLdX ? (const R*)args.dLdX + (size_t)pid * (T + 1) * NX : nullptr;
   const R* sUg = args.dLdU ? (const R*)args.dLdU + (size_t)pid * T * NU : nullptr;
   const R sJ = args.dLdJ ? ((const R*)args.dLdJ)[pid] : R(0);
+  CostPipe<M, DIAG, R, G> ricp{&S, Cg, nullptr, T, lane, -1};
+  CostPipe<M, DIAG, R, G> adjp{&S, Cg, cg, T, lane, -1};
   const bool want_theta = args.dtheta != nullptr && args.n_theta > 0;
   const bool want_adjoint = want_theta || sJ != R(0);
 
   const R* thg = (const R*)args.theta + (size_t)args.theta_stride * pid;
-  R th_r[NTHL];
+  R* P_r = (R*)(base + L.oPr);
   if constexpr (!M::kLinearParams) {
+    if (lane == 0) {
+      R th_r[M::NTH > 0 ? M::NTH : 1], pr[M::NP];
 #pragma unroll
-    for (int i = 0; i < NTHL; i++) th_r[i] = (i < M::NTH) ? thg[i] : R(0);
-  } else {
-    th_r[0] = R(0);
+      for (int i = 0; i < M::NTH; i++) th_r[i] = thg[i];
+      M::template prep<R>(th_r, pr);
+#pragma unroll
+      for (int i = 0; i < M::NP; i++) P_r[i] = pr[i];
+    }
+    __syncwarp(gm);
   }
   const R dt_r = (R)args.dt;
   if constexpr (M::kLinearParams) {
-    for (int e = lane; e < NX * NX; e += G) As[(e / NX) * LDA + e % NX] = thg[e];
-    for (int e = lane; e < NX * NU; e += G) Bs[e] = thg[NX * NX + e];
+    for (int e = lane; e < NX * NX; e += G) S.As[(e / NX) * LDA + e % NX] = thg[e];
+    for (int e = lane; e < NX * NU; e += G) S.Bs[(e / NU) * LDB + e % NU] = thg[NX * NX + e];
   } else {
-    M::template jac_const<R>(th_r, dt_r, As, LDA, Bs, lane, G);
+    M::template jac_const<R>(P_r, dt_r, S.As, LDA, S.Bs, LDB, lane, G);
   }
   {
     const R* xg = (const R*)args.X + (size_t)pid * (T + 1) * NX;
     for (int e = lane; e < (T + 1) * NX; e += G) {
-      Xs[e] = xg[e];
-      dXs[e] = R(0);
+      const int t = e / NX, i = e % NX;
+      Xs[t * LDA + i] = xg[e];
+      dXs[t * LDA + i] = R(0);
     }
     const R* ug = (const R*)args.U + (size_t)pid * T * NU;
     for (int e = lane; e < T * NU; e += G) {
       const R v = ug[e];
-      const int r = e % NU;
-      Us[e] = v;
-      dUs[e] = R(0);
+      const int t = e / NU, r = e % NU;
+      Us[t * LDB + r] = v;
+      dUs[t * LDB + r] = R(0);
       // clamped = (U <= u_min) | (U >= u_max)  (policy.py:271)
       cl[e] = (uint8_t)((double)v <= args.u_min[r] || (double)v >= args.u_max[r]);
     }
   }
-  auto stage_C = [&](int t, int buf) {
-    const R* src = Cg + (size_t)t * NCS;
-    R* dst = Cb + buf * NCS;
-    for (int e = lane; e < NCS; e += G) cp_async_elem(dst + e, src + e);
-    if (cg) {
-      const R* s2 = cg + (size_t)t * NZ;
-      R* d2 = cb + buf * NZ;
-      for (int e = lane; e < NZ; e += G) cp_async_elem(d2 + e, s2 + e);
-    }
-    cp_async_commit();
-  };
-  auto load_z = [&](int t, R (&xr)[NX], R (&ur)[NU]) {
-#pragma unroll
-    for (int i = 0; i < NX; i++) xr[i] = Xs[t * NX + i];
-#pragma unroll
-    for (int i = 0; i < NU; i++) ur[i] = Us[t * NU + i];
-  };
   // V_x = dL/dX_T, V_xx = 0 (gradlayer.py:106-107)
-  for (int e = lane; e < NX; e += G) Vxs[e] = sXg ? sXg[T * NX + e] : R(0);
+  for (int e = lane; e < NX; e += G) S.Vx[e] = sXg ? sXg[T * NX + e] : R(0);
   __syncwarp(gm);
 
   // ======================= auxiliary Riccati sweep (kernels.py:582-707) =========
@@ -179,110 +149,55 @@ __global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) 
     R vxx[NX];
 #pragma unroll
     for (int b = 0; b < NX; b++) vxx[b] = R(0);
-    stage_C(T - 1, (T - 1) & 1);
+    ricp.start(T - 1);
     for (int t = T - 1; t >= 0; t--) {
-      const int buf = t & 1;
-      if (t > 0) {
-        stage_C(t - 1, buf ^ 1);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      } else {
-        cp_async_wait_all();
-      }
-      const R* Cs = Cb + buf * NCS;
+      ricp.acquire(t);
+      const R* Cs = ricp.C(t);
       R xr[NX], ur[NU];
-      load_z(t, xr, ur);
+      lds_row<NX>(Xs + t * LDA, xr);
+      lds_row<NU>(Us + t * LDB, ur);
       __syncwarp(gm);
-      if constexpr (!M::kLinearParams) M::template jac_vary<R>(th_r, dt_r, xr, ur, As, LDA, Bs);
+      if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
       __syncwarp(gm);
       R qx = R(0);
+      R vx[NX];
+      lds_row<NX>(S.Vx, vx);
       if (lane < NX) {
         const int a = lane;
         R s = sXg ? sXg[t * NX + a] : R(0);
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += As[b * LDA + a] * Vxs[b];
+        for (int b = 0; b < NX; b++) s += S.As[b * LDA + a] * vx[b];
         qx = s;
       }
       if (lane < NU) {
         const int a = lane;
         R s = sUg ? sUg[t * NU + a] : R(0);
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += Bs[b * NU + a] * Vxs[b];
-        qus[a] = s;
+        for (int b = 0; b < NX; b++) s += S.Bs[b * LDB + a] * vx[b];
+        S.qu[a] = s;
       }
-      if (lane < NX) {
-        R ma[NX], nb[NU];
-#pragma unroll
-        for (int b = 0; b < NX; b++) ma[b] = R(0);
-#pragma unroll
-        for (int b = 0; b < NU; b++) nb[b] = R(0);
-#pragma unroll
-        for (int r = 0; r < NX; r++) {
-          const R v = vxx[r];
-#pragma unroll
-          for (int b = 0; b < NX; b++) ma[b] += v * As[r * LDA + b];
-#pragma unroll
-          for (int b = 0; b < NU; b++) nb[b] += v * Bs[r * NU + b];
-        }
-#pragma unroll
-        for (int b = 0; b < NX; b++) MA[lane * LDA + b] = ma[b];
-#pragma unroll
-        for (int b = 0; b < NU; b++) NB[lane * NU + b] = nb[b];
-      }
+      if (lane < NX) ric_MA_NB<M, DIAG, R>(S, lane, vxx);
       __syncwarp(gm);
-      // Quu (all lanes, redundantly, into registers), Qux column, Qxx row
-      R quu[NU][NU];
-#pragma unroll
-      for (int i = 0; i < NU; i++)
-#pragma unroll
-        for (int j = 0; j < NU; j++) {
-          R s;
-          if constexpr (DIAG) {
-            s = (i == j) ? Cs[NX + i] : R(0);
-          } else {
-            s = Cs[(NX + i) * NZ + NX + j];
-          }
-#pragma unroll
-          for (int r = 0; r < NX; r++) s += Bs[r * NU + i] * NB[r * NU + j];
-          quu[i][j] = s;
-        }
+      for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU);
       R quxc[NU], qxx[NX];
-      if (lane < NX) {
-        const int b = lane;
-#pragma unroll
-        for (int i = 0; i < NU; i++) {
-          R s;
-          if constexpr (DIAG) {
-            s = R(0);
-          } else {
-            s = Cs[(NX + i) * NZ + b];
-          }
-#pragma unroll
-          for (int r = 0; r < NX; r++) s += Bs[r * NU + i] * MA[r * LDA + b];
-          quxc[i] = s;
-        }
-        const int a = lane;
-#pragma unroll
-        for (int bb = 0; bb < NX; bb++) {
-          if constexpr (DIAG) {
-            qxx[bb] = (bb == a) ? Cs[a] : R(0);
-          } else {
-            qxx[bb] = Cs[a * NZ + bb];
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < NX; r++) {
-          const R ar = As[r * LDA + a];
-#pragma unroll
-          for (int bb = 0; bb < NX; bb++) qxx[bb] += ar * MA[r * LDA + bb];
-        }
-      }
+      if (lane < NX) ric_Qxx_Qux<M, DIAG, R>(S, Cs, lane, qxx, quxc);
+      __syncwarp(gm);
+      ricp.release(t);
       // freeze clamped dimensions (kernels.py:658-667)
-      R qu[NU];
+      R quu[NU][NU], qu[NU];
+      bool clm[NU];
 #pragma unroll
-      for (int i = 0; i < NU; i++) qu[i] = qus[i];
+      for (int i = 0; i < NU; i++) {
+        R qrow[NU];
+        lds_row<NU>(S.Quu + i * LDB, qrow);
+#pragma unroll
+        for (int j = 0; j < NU; j++) quu[i][j] = qrow[j];
+        qu[i] = S.qu[i];
+        clm[i] = cl[t * NU + i] != 0;
+      }
 #pragma unroll
       for (int a = 0; a < NU; a++) {
-        if (cl[t * NU + a]) {
+        if (clm[a]) {
           qu[a] = R(0);
           quxc[a] = R(0);
 #pragma unroll
@@ -293,56 +208,37 @@ __global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) 
           quu[a][a] = R(1);
         }
       }
-      __syncwarp(gm);
-      // full m x m Cholesky (double) and the gains k = -Quu^-1 qu, K = -Quu^-1 Qux
-      double Hd[NU][NU];
+      // full m x m Cholesky and the gains k = -Quu^-1 qu, K = -Quu^-1 Qux
       bool allf[NU];
 #pragma unroll
-      for (int i = 0; i < NU; i++) {
-        allf[i] = true;
-#pragma unroll
-        for (int j = 0; j < NU; j++) Hd[i][j] = (double)quu[i][j];
-      }
-      Chol<NU> ch;
-      if (!chol_masked<NU>(Hd, allf, ch)) {
+      for (int i = 0; i < NU; i++) allf[i] = true;
+      Chol<NU, R> ch;
+      if (!chol_masked<NU, R>(quu, R(0), allf, ch)) {
         fail_t = t;
         break;
       }
       R kt[NU];
       {
-        double rhs[NU], sol[NU];
+        R sol[NU];
+        chol_solve<NU, R>(ch, qu, sol);
 #pragma unroll
-        for (int i = 0; i < NU; i++) rhs[i] = (double)qu[i];
-        chol_solve<NU>(ch, rhs, sol);
-#pragma unroll
-        for (int i = 0; i < NU; i++) kt[i] = (R)(-sol[i]);
+        for (int i = 0; i < NU; i++) kt[i] = -sol[i];
       }
-      if (lane < NU) {
+      if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < NU; i++)
-          if (i == lane) ka[t * NU + i] = kt[i];
+        for (int i = 0; i < NU; i++) ka[t * LDB + i] = kt[i];
       }
       R kcol[NU];
       if (lane < NX) {
         const int b = lane;
-        double rhs[NU], sol[NU];
-#pragma unroll
-        for (int i = 0; i < NU; i++) rhs[i] = (double)quxc[i];
-        chol_solve<NU>(ch, rhs, sol);
+        R sol[NU];
+        chol_solve<NU, R>(ch, quxc, sol);
 #pragma unroll
         for (int i = 0; i < NU; i++) {
-          kcol[i] = (R)(-sol[i]);
-          Ka[(t * NU + i) * NX + b] = kcol[i];
-          KT[b * NU + i] = kcol[i];
-          QuxT[b * NU + i] = quxc[i];
+          kcol[i] = -sol[i];
+          Ka[(t * NU + i) * LDA + b] = kcol[i];
         }
-#pragma unroll
-        for (int i = 0; i < NU; i++) {
-          R s = R(0);
-#pragma unroll
-          for (int q = 0; q < NU; q++) s += quu[i][q] * kcol[q];
-          QuuKT[b * NU + i] = s;
-        }
+        ric_publish_cols<M, DIAG, R>(S, b, kcol, quxc, quu);
         R s = qx;
 #pragma unroll
         for (int r = 0; r < NU; r++) {
@@ -351,40 +247,24 @@ __global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) 
           for (int q = 0; q < NU; q++) rowq += quu[r][q] * kt[q];
           s += kcol[r] * (rowq + qu[r]) + quxc[r] * kt[r];
         }
-        Vxs[b] = s;
+        S.Vx[b] = s;
       }
       __syncwarp(gm);
-      if (lane < NX) {
-        const int a = lane;
-#pragma unroll
-        for (int bb = 0; bb < NX; bb++) {
-          R s = qxx[bb];
-#pragma unroll
-          for (int r = 0; r < NU; r++) {
-            const R Kra = kcol[r], Qra = quxc[r];
-            s += (Kra * QuuKT[bb * NU + r] + Kra * QuxT[bb * NU + r]) + Qra * KT[bb * NU + r];
-          }
-          MA[a * LDA + bb] = s;
-        }
-      }
+      if (lane < NX) ric_Vxx_row<M, DIAG, R>(S, lane, qxx, kcol, quxc);
       __syncwarp(gm);
-      if (lane < NX) {
-        const int a = lane;
-#pragma unroll
-        for (int bb = 0; bb < NX; bb++) vxx[bb] = R(0.5) * (MA[a * LDA + bb] + MA[bb * LDA + a]);
-      }
+      if (lane < NX) ric_symmetrize<M, DIAG, R>(S, lane, vxx);
     }
     cp_async_wait_all();
     __syncwarp(gm);
   }
 
   const bool failed = fail_t >= 0;
-  R* dCo = args.dC ? (R*)args.dC + (size_t)pid * T * (DIAG ? NZ : NZ * NZ) : nullptr;
+  R* dCo = args.dC ? (R*)args.dC + (size_t)pid * T * D::NCS : nullptr;
   R* dco = args.dc ? (R*)args.dc + (size_t)pid * T * NZ : nullptr;
   if (failed) {
     // failed instances get zero gradients (gradlayer.py:153-159, policy.py:277-280)
     if (dCo)
-      for (int e = lane; e < T * (DIAG ? NZ : NZ * NZ); e += G) dCo[e] = R(0);
+      for (int e = lane; e < T * D::NCS; e += G) dCo[e] = R(0);
     if (dco)
       for (int e = lane; e < T * NZ; e += G) dco[e] = R(0);
     if (args.dx0)
@@ -395,35 +275,42 @@ __global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) 
     // ============ differential rollout + assembly (kernels.py:710-756) ============
     for (int t = 0; t < T; t++) {
       R xr[NX], ur[NU];
-      load_z(t, xr, ur);
-      if constexpr (!M::kLinearParams) M::template jac_vary<R>(th_r, dt_r, xr, ur, As, LDA, Bs);
+      lds_row<NX>(Xs + t * LDA, xr);
+      lds_row<NU>(Us + t * LDB, ur);
+      if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
+      R dx[NX];
+      lds_row<NX>(dXs + t * LDA, dx);
       if (lane < NU) {
         const int r = lane;
-        R s = ka[t * NU + r];
+        R s = ka[t * LDB + r];
+        R krow[NX];
+        lds_row<NX>(Ka + (t * NU + r) * LDA, krow);
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += Ka[(t * NU + r) * NX + b] * dXs[t * NX + b];
-        dUs[t * NU + r] = s;
+        for (int b = 0; b < NX; b++) s += krow[b] * dx[b];
+        dUs[t * LDB + r] = s;
       }
       __syncwarp(gm);
+      R du[NU];
+      lds_row<NU>(dUs + t * LDB, du);
       if (lane < NX) {
         const int a = lane;
+        R arow[NX], brow[NU];
+        lds_row<NX>(S.As + a * LDA, arow);
+        lds_row<NU>(S.Bs + a * LDB, brow);
         R s = R(0);
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += As[a * LDA + b] * dXs[t * NX + b];
+        for (int b = 0; b < NX; b++) s += arow[b] * dx[b];
 #pragma unroll
-        for (int b = 0; b < NU; b++) s += Bs[a * NU + b] * dUs[t * NU + b];
-        dXs[(t + 1) * NX + a] = s;
+        for (int b = 0; b < NU; b++) s += brow[b] * du[b];
+        dXs[(t + 1) * LDA + a] = s;
       }
       // assembly of stage t: dc = dz, dC = 0.5 (dz z' + z dz'), clamped rows/cols zero;
       // plus the optimal-cost terms sJ z and sJ/2 z z'
-      auto zat = [&](int a) -> R { return a < NX ? Xs[t * NX + a] : Us[t * NU + a - NX]; };
-      auto dzat = [&](int a) -> R { return a < NX ? dXs[t * NX + a] : dUs[t * NU + a - NX]; };
+      auto zat = [&](int a) -> R { return a < NX ? Xs[t * LDA + a] : Us[t * LDB + a - NX]; };
+      auto dzat = [&](int a) -> R { return a < NX ? dXs[t * LDA + a] : dUs[t * LDB + a - NX]; };
       auto clat = [&](int a) -> bool { return a >= NX && cl[t * NU + a - NX]; };
       if (dco) {
-        for (int a = lane; a < NZ; a += G) {
-          const R za = zat(a);
-          dco[t * NZ + a] = (clat(a) ? R(0) : dzat(a)) + sJ * za;
-        }
+        for (int a = lane; a < NZ; a += G) dco[t * NZ + a] = (clat(a) ? R(0) : dzat(a)) + sJ * zat(a);
       }
       if (dCo) {
         if constexpr (DIAG) {
@@ -445,9 +332,9 @@ __global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) 
     }
 
     // ============ co-state recursions: dtheta and the envelope terms (NEW) ========
-    R gth[NTHL];
+    R gth[M::NTH > 0 && !M::kLinearParams ? M::NTH : 1];
 #pragma unroll
-    for (int i = 0; i < NTHL; i++) gth[i] = R(0);
+    for (int i = 0; i < (M::NTH > 0 && !M::kLinearParams ? M::NTH : 1); i++) gth[i] = R(0);
     constexpr int NZL = M::kLinearParams ? NZ : 1;
     R grow[NZL];  // linear model: row `lane` of [dA | dB]
 #pragma unroll
@@ -457,72 +344,68 @@ __global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) 
         lams[e] = R(0);
         lhs[e] = sXg ? sXg[T * NX + e] : R(0);
       }
-      stage_C(T - 1, (T - 1) & 1);
+      adjp.start(T - 1);
       for (int t = T - 1; t >= 0; t--) {
-        const int buf = t & 1;
-        if (t > 0) {
-          stage_C(t - 1, buf ^ 1);
-          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        } else {
-          cp_async_wait_all();
-        }
-        R xr[NX], ur[NU];
-        load_z(t, xr, ur);
+        adjp.acquire(t);
+        R xr[NX], ur[NU], dx[NX], du[NU], lm[NX], lh[NX];
+        lds_row<NX>(Xs + t * LDA, xr);
+        lds_row<NU>(Us + t * LDB, ur);
+        lds_row<NX>(dXs + t * LDA, dx);
+        lds_row<NU>(dUs + t * LDB, du);
+        lds_row<NX>(lams, lm);
+        lds_row<NX>(lhs, lh);
         __syncwarp(gm);
-        if constexpr (!M::kLinearParams) M::template jac_vary<R>(th_r, dt_r, xr, ur, As, LDA, Bs);
+        if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
         __syncwarp(gm);
         if (want_theta) {
           if constexpr (M::kLinearParams) {
             if (lane < NX) {
               const int i = lane;
-              const R lh = lhs[i], lm = lams[i], ls = sJ * lams[i];
+              const R lhi = lhs[i], lmi = lams[i], lsi = sJ * lams[i];
 #pragma unroll
-              for (int j = 0; j < NX; j++) grow[j] += lh * xr[j] + lm * dXs[t * NX + j] + ls * xr[j];
+              for (int j2 = 0; j2 < NX; j2++) grow[j2] += lhi * xr[j2] + lmi * dx[j2] + lsi * xr[j2];
 #pragma unroll
-              for (int j = 0; j < NU; j++) grow[NX + j] += lh * ur[j] + lm * dUs[t * NU + j] + ls * ur[j];
+              for (int j2 = 0; j2 < NU; j2++) grow[NX + j2] += lhi * ur[j2] + lmi * du[j2] + lsi * ur[j2];
             }
-          } else {
-            R dx[NX], du[NU], lh[NX], lm[NX];
+          } else if constexpr (M::NTH > 0) {
+            R lhe[NX];
 #pragma unroll
-            for (int i = 0; i < NX; i++) {
-              dx[i] = dXs[t * NX + i];
-              lh[i] = lhs[i] + sJ * lams[i];
-              lm[i] = lams[i];
-            }
-#pragma unroll
-            for (int i = 0; i < NU; i++) du[i] = dUs[t * NU + i];
-            M::template theta_grad<R>(th_r, dt_r, xr, ur, dx, du, lh, lm, gth);
+            for (int i = 0; i < NX; i++) lhe[i] = lh[i] + sJ * lm[i];
+            M::template theta_grad<R>(P_r, dt_r, xr, ur, dx, du, lhe, lm, gth);
           }
         }
-        const R* Cs = Cb + buf * NCS;
-        const R* cs = cb + buf * NZ;
+        const R* Cs = adjp.C(t);
+        const R* cs = adjp.c(t);
         R nl = R(0), nh = R(0);
         if (lane < NX) {
           const int a = lane;
           R s1 = cg ? cs[a] : R(0);
           R s2 = sXg ? sXg[t * NX + a] : R(0);
           if constexpr (DIAG) {
-            const R za = Xs[t * NX + a];
-            s1 += Cs[a] * za;
-            s2 += Cs[a] * dXs[t * NX + a];
+            s1 += Cs[a] * Xs[t * LDA + a];
+            s2 += Cs[a] * dXs[t * LDA + a];
           } else {
+            R crow[NZ];
+            lds_row<NZ>(Cs + a * ZLD, crow);
 #pragma unroll
             for (int b = 0; b < NZ; b++) {
               const R zb = b < NX ? xr[b < NX ? b : 0] : ur[b >= NX ? b - NX : 0];
-              const R db = b < NX ? dXs[t * NX + b] : dUs[t * NU + b - NX];
-              s1 += Cs[a * NZ + b] * zb;
-              s2 += Cs[a * NZ + b] * db;
+              const R db = b < NX ? dx[b < NX ? b : 0] : du[b >= NX ? b - NX : 0];
+              s1 += crow[b] * zb;
+              s2 += crow[b] * db;
             }
           }
 #pragma unroll
           for (int b = 0; b < NX; b++) {
-            s1 += As[b * LDA + a] * lams[b];
-            s2 += As[b * LDA + a] * lhs[b];
+            const R ab = S.As[b * LDA + a];
+            s1 += ab * lm[b];
+            s2 += ab * lh[b];
           }
           nl = s1;
           nh = s2;
         }
         __syncwarp(gm);
+        adjp.release(t);
         if (lane < NX) {
           lams[lane] = nl;
           lhs[lane] = nh;
@@ -534,27 +417,29 @@ __global__ void __launch_bounds__(128) ilqr_backward_kernel(const BwdArgs args) 
     }
     if (args.dx0) {
       R* o = (R*)args.dx0 + (size_t)pid * NX;
-      for (int e = lane; e < NX; e += G) o[e] = Vxs[e] + (want_adjoint ? sJ * lams[e] : R(0));
+      for (int e = lane; e < NX; e += G) o[e] = S.Vx[e] + (want_adjoint ? sJ * lams[e] : R(0));
     }
     if (want_theta) {
       R* o = (R*)args.dtheta + (size_t)pid * args.n_theta;
       if constexpr (M::kLinearParams) {
         if (lane < NX) {
 #pragma unroll
-          for (int j = 0; j < NX; j++) o[lane * NX + j] = grow[j];
+          for (int j2 = 0; j2 < NX; j2++) o[lane * NX + j2] = grow[j2];
 #pragma unroll
-          for (int j = 0; j < NU; j++) o[NX * NX + lane * NU + j] = grow[NX + j];
+          for (int j2 = 0; j2 < NU; j2++) o[NX * NX + lane * NU + j2] = grow[NX + j2];
         }
-      } else {
+      } else if constexpr (M::NTH > 0) {
         if (lane == 0)
           for (int i = 0; i < M::NTH; i++) o[i] = gth[i];
       }
     }
   }
   if (args.dX)
-    for (int e = lane; e < (T + 1) * NX; e += G) ((R*)args.dX)[(size_t)pid * (T + 1) * NX + e] = dXs[e];
+    for (int e = lane; e < (T + 1) * NX; e += G)
+      ((R*)args.dX)[(size_t)pid * (T + 1) * NX + e] = dXs[(e / NX) * LDA + e % NX];
   if (args.dU)
-    for (int e = lane; e < T * NU; e += G) ((R*)args.dU)[(size_t)pid * T * NU + e] = dUs[e];
+    for (int e = lane; e < T * NU; e += G)
+      ((R*)args.dU)[(size_t)pid * T * NU + e] = dUs[(e / NU) * LDB + e % NU];
   if (args.fail_t && lane == 0) args.fail_t[pid] = fail_t;
 }
 

@@ -27,7 +27,7 @@
 #pragma once
 #include <type_traits>
 
-#include "common.cuh"
+#include "riccati.cuh"
 
 namespace dmpc {
 
@@ -58,64 +58,56 @@ __host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a *
 
 template <class M, bool DIAG, class R>
 struct FwdLayout {
-  static constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
-  static constexpr int LDA = NX;
-  static constexpr int NCS = DIAG ? NZ : NZ * NZ;
-  int oXn, oUn, okg, oKg, oAs, oBs, oMA, oNB, oKT, oQuxT, oQuuKT, oQuu, oqu, oVx, ozs, oC, oc, total;
+  using D = Dims<M, DIAG, R>;
+  int oPe, oPr, oXn, oUn, okg, oKg, total;
+  RicLayout<M, DIAG, R> ric;
   __host__ __device__ static FwdLayout make(int T) {
     FwdLayout L;
     int o = 0;
-    L.oXn = o; o += (T + 1) * NX * 8;
-    L.oUn = o; o += T * NU * 8;
-    L.okg = o; o += T * NU * 8;
-    L.oKg = o; o += T * NU * NX * (int)sizeof(R);
+    L.oPe = o; o += align_up(M::NP * 8, 16);
+    L.oPr = o; o += align_up(M::NP * (int)sizeof(R), 16);
+    L.oXn = o; o += (T + 1) * D::XLD * 8;
+    L.oUn = o; o += T * D::ULD * 8;
+    L.okg = o; o += T * D::ULD * 8;
     o = align_up(o, 16);
-    L.oAs = o; o += NX * LDA * (int)sizeof(R);
-    L.oBs = o; o += NX * NU * (int)sizeof(R);
-    L.oMA = o; o += NX * LDA * (int)sizeof(R);
-    L.oNB = o; o += NX * NU * (int)sizeof(R);
-    L.oKT = o; o += NX * NU * (int)sizeof(R);
-    L.oQuxT = o; o += NX * NU * (int)sizeof(R);
-    L.oQuuKT = o; o += NX * NU * (int)sizeof(R);
-    L.oQuu = o; o += NU * NU * (int)sizeof(R);
-    L.oqu = o; o += NU * (int)sizeof(R);
-    L.oVx = o; o += NX * (int)sizeof(R);
-    L.ozs = o; o += NZ * (int)sizeof(R);
+    L.oKg = o; o += T * D::NU * D::LDA * (int)sizeof(R);
     o = align_up(o, 16);
-    L.oC = o; o += 2 * NCS * (int)sizeof(R);
-    L.oc = o; o += 2 * NZ * (int)sizeof(R);
-    L.total = align_up(o, 16);
+    L.ric = RicLayout<M, DIAG, R>::make(o);
+    L.total = align_up(L.ric.end, 16);
     return L;
   }
 };
 
 // x+ = f(x,u) in double; the linear model reads its [A|B] copy from shared memory.
 template <class M, class R>
-DMPC_DEV void step_e(const double* th, double dt, const R* As, const R* Bs, const double* x,
-                     const double* u, double* o) {
+DMPC_DEV void step_e(const double* P, double dt, const R* As, int lda, const R* Bs, int ldb,
+                     const double* x, const double* u, double* o) {
   if constexpr (M::kLinearParams) {
 #pragma unroll
     for (int i = 0; i < M::NX; i++) {
+      R arow[M::NX], brow[M::NU];
+      lds_row<M::NX>(As + i * lda, arow);
+      lds_row<M::NU>(Bs + i * ldb, brow);
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < M::NX; j++) acc += (double)As[i * M::NX + j] * x[j];
+      for (int j = 0; j < M::NX; j++) acc += (double)arow[j] * x[j];
 #pragma unroll
-      for (int j = 0; j < M::NU; j++) acc += (double)Bs[i * M::NU + j] * u[j];
+      for (int j = 0; j < M::NU; j++) acc += (double)brow[j] * u[j];
       o[i] = acc;
     }
   } else {
-    M::template step<double>(th, dt, x, u, o);
+    M::template step<double>(P, dt, x, u, o);
   }
 }
 
 template <class M, int G, bool DIAG, class R>
-__global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2) ilqr_forward_kernel(const FwdArgs args) {
+  using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
-  using Lay = FwdLayout<M, DIAG, R>;
-  constexpr int LDA = Lay::LDA, NCS = Lay::NCS;
+  constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD, XLD = D::XLD, ULD = D::ULD;
   constexpr int NSLOT = G >= 4 ? 4 : G;  // concurrent line-search candidates
   constexpr int LC = G / NSLOT;          // lanes per candidate slot
-  constexpr int NTHL = M::kLinearParams ? 1 : (M::NTH > 0 ? M::NTH : 1);
+  using Lay = FwdLayout<M, DIAG, R>;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
@@ -130,84 +122,68 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
   double* Un = (double*)(base + L.oUn);
   double* kg = (double*)(base + L.okg);
   R* Kg = (R*)(base + L.oKg);
-  R* As = (R*)(base + L.oAs);
-  R* Bs = (R*)(base + L.oBs);
-  R* MA = (R*)(base + L.oMA);
-  R* NB = (R*)(base + L.oNB);
-  R* KT = (R*)(base + L.oKT);
-  R* QuxT = (R*)(base + L.oQuxT);
-  R* QuuKT = (R*)(base + L.oQuuKT);
-  R* Quus = (R*)(base + L.oQuu);
-  R* qus = (R*)(base + L.oqu);
-  R* Vxs = (R*)(base + L.oVx);
-  R* zs = (R*)(base + L.ozs);
-  R* Cb = (R*)(base + L.oC);
-  R* cb = (R*)(base + L.oc);
+  Ric<M, DIAG, R> S;
+  S.bind(base, L.ric);
 
-  const R* Cg = (const R*)args.C + (size_t)pid * T * NCS;
+  const R* Cg = (const R*)args.C + (size_t)pid * T * D::NCS;
   const R* cg = (const R*)args.c + (size_t)pid * T * NZ;
+  CostPipe<M, DIAG, R, G> fwdp{&S, Cg, cg, T, lane, +1};
+  CostPipe<M, DIAG, R, G> bwdp{&S, Cg, cg, T, lane, -1};
 
-  // ---- parameters ----
+  // ---- parameters (prepared: raw + reciprocals), kept in shared memory ----
   const R* thg = (const R*)args.theta + (size_t)args.theta_stride * pid;
-  double th_e[NTHL];
-  R th_r[NTHL];
+  double* P_e = (double*)(base + L.oPe);
+  R* P_r = (R*)(base + L.oPr);
   if constexpr (!M::kLinearParams) {
+    if (lane == 0) {
+      double th_e[M::NTH > 0 ? M::NTH : 1], pe[M::NP];
+      R th_r[M::NTH > 0 ? M::NTH : 1], pr[M::NP];
 #pragma unroll
-    for (int i = 0; i < NTHL; i++) {
-      th_r[i] = (i < M::NTH) ? thg[i] : R(0);
-      th_e[i] = (double)th_r[i];
+      for (int i = 0; i < M::NTH; i++) {
+        th_r[i] = thg[i];
+        th_e[i] = (double)th_r[i];
+      }
+      M::template prep<double>(th_e, pe);
+      M::template prep<R>(th_r, pr);
+#pragma unroll
+      for (int i = 0; i < M::NP; i++) {
+        P_e[i] = pe[i];
+        P_r[i] = pr[i];
+      }
     }
-  } else {
-    th_e[0] = 0.0;
-    th_r[0] = R(0);
+    __syncwarp(gm);
   }
   const double dt_e = args.dt;
   const R dt_r = (R)args.dt;
 
   // ---- constant Jacobian structure (written once) ----
   if constexpr (M::kLinearParams) {
-    for (int e = lane; e < NX * NX; e += G) As[(e / NX) * LDA + e % NX] = thg[e];
-    for (int e = lane; e < NX * NU; e += G) Bs[e] = thg[NX * NX + e];
+    for (int e = lane; e < NX * NX; e += G) S.As[(e / NX) * LDA + e % NX] = thg[e];
+    for (int e = lane; e < NX * NU; e += G) S.Bs[(e / NU) * LDB + e % NU] = thg[NX * NX + e];
   } else {
-    M::template jac_const<R>(th_r, dt_r, As, LDA, Bs, lane, G);
+    M::template jac_const<R>(P_r, dt_r, S.As, LDA, S.Bs, LDB, lane, G);
   }
 
   // ---- load x0, U_warm (clipped, ilqr.py:165); zero K, k (Workspace init) ----
-  double umin[NU], umax[NU];
-#pragma unroll
-  for (int r = 0; r < NU; r++) {
-    umin[r] = args.u_min[r];
-    umax[r] = args.u_max[r];
-  }
   {
     const R* xg = (const R*)args.x0 + (size_t)pid * NX;
     for (int e = lane; e < NX; e += G) Xn[e] = (double)xg[e];
     const R* ug = (const R*)args.U_warm + (size_t)pid * T * NU;
     for (int e = lane; e < T * NU; e += G) {
       double v = (double)ug[e];
-      const int r = e % NU;
+      const int t = e / NU, r = e % NU;
       const double lo = args.u_min[r], hi = args.u_max[r];
       v = v < lo ? lo : v;  // np.clip
       v = v > hi ? hi : v;
-      Un[e] = v;
-      kg[e] = 0.0;
+      Un[t * ULD + r] = v;
+      kg[t * ULD + r] = 0.0;
     }
-    for (int e = lane; e < T * NU * NX; e += G) Kg[e] = R(0);
+    for (int e = lane; e < T * NU * LDA; e += G) Kg[e] = R(0);
   }
   __syncwarp(gm);
 
-  auto stage_C = [&](int t, int buf) {
-    const R* src = Cg + (size_t)t * NCS;
-    R* dst = Cb + buf * NCS;
-    for (int e = lane; e < NCS; e += G) cp_async_elem(dst + e, src + e);
-    const R* s2 = cg + (size_t)t * NZ;
-    R* d2 = cb + buf * NZ;
-    for (int e = lane; e < NZ; e += G) cp_async_elem(d2 + e, s2 + e);
-    cp_async_commit();
-  };
-
-  // stage cost 0.5 z'Cz + c'z of a trajectory point in double; rows of the dense
-  // quadratic form are split over the LCX lanes of a slot (j = lane in slot) and
+  // stage cost 0.5 z'Cz + c'z in double (_stage_cost_xu, kernels.py:133-145); rows of the
+  // dense quadratic form are split over the LCX lanes of a slot (j = lane in slot) and
   // reduced with xor shuffles (every lane ends with the identical sum).
   auto stage_cost = [&](auto lcx_tag, const R* Cs, const R* cs, const double* x, const double* u,
                         int j, unsigned smask) -> double {
@@ -219,9 +195,11 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
     for (int i = 0; i < NU; i++) z[NX + i] = u[i];
     double part = 0.0;
     if constexpr (DIAG) {
-      // _stage_cost_xu with a diagonal C: row_i = d_i z_i (kernels.py:133-145)
+      R d[NZ], cc[NZ];
+      lds_row<NZ>(Cs, d);
+      lds_row<NZ>(cs, cc);
 #pragma unroll
-      for (int i = 0; i < NZ; i++) part += 0.5 * z[i] * ((double)Cs[i] * z[i]) + (double)cs[i] * z[i];
+      for (int i = 0; i < NZ; i++) part += 0.5 * z[i] * ((double)d[i] * z[i]) + (double)cc[i] * z[i];
       return part;
     } else {
       constexpr int NR = (NZ + LCX - 1) / LCX;
@@ -229,10 +207,11 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
       for (int m = 0; m < NR; m++) {
         const int i = j + m * LCX;
         if (i < NZ) {
+          R crow[NZ];
+          lds_row<NZ>(Cs + i * ZLD, crow);
           double row = 0.0;
-          const R* Ci = Cs + i * NZ;
 #pragma unroll
-          for (int jj = 0; jj < NZ; jj++) row += (double)Ci[jj] * z[jj];
+          for (int jj = 0; jj < NZ; jj++) row += (double)crow[jj] * z[jj];
           double zi = 0.0;
 #pragma unroll
           for (int k = 0; k < LCX; k++)
@@ -256,24 +235,18 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
   // =========================== initial rollout (kernels.py:161-178) ===========
   {
     double xc[NX];
-#pragma unroll
-    for (int i = 0; i < NX; i++) xc[i] = Xn[i];
-    stage_C(0, 0);
+    lds_row_d<NX>(Xn, xc);
+    fwdp.start(0);
     for (int t = 0; t < T; t++) {
-      const int buf = t & 1;
-      if (t + 1 < T) {
-        stage_C(t + 1, buf ^ 1);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      } else {
-        cp_async_wait_all();
-      }
+      fwdp.acquire(t);
       __syncwarp(gm);
       double u[NU];
-#pragma unroll
-      for (int r = 0; r < NU; r++) u[r] = Un[t * NU + r];
-      J += stage_cost(std::integral_constant<int, G>{}, Cb + buf * NCS, cb + buf * NZ, xc, u, lane, gm);
+      lds_row_d<NU>(Un + t * ULD, u);
+      J += stage_cost(std::integral_constant<int, G>{}, fwdp.C(t), fwdp.c(t), xc, u, lane, gm);
+      __syncwarp(gm);
+      fwdp.release(t);
       double xn[NX];
-      step_e<M, R>(th_e, dt_e, As, Bs, xc, u, xn);
+      step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
       bool fin = true;
 #pragma unroll
       for (int i = 0; i < NX; i++) {
@@ -282,7 +255,7 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
       }
 #pragma unroll
       for (int i = 0; i < NX; i++)
-        if ((i % G) == lane) Xn[(t + 1) * NX + i] = xn[i];
+        if ((i % G) == lane) Xn[(t + 1) * XLD + i] = xn[i];
       __syncwarp(gm);
       if (!fin) {
         fail_t = t;
@@ -304,207 +277,119 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
     R vxx[NX];  // row `lane` of V_xx (value Hessian), carried across stages
 #pragma unroll
     for (int b = 0; b < NX; b++) vxx[b] = R(0);
-    for (int e = lane; e < NX; e += G) Vxs[e] = R(0);
-    stage_C(T - 1, (T - 1) & 1);
+    for (int e = lane; e < NX; e += G) S.Vx[e] = R(0);
+    bwdp.start(T - 1);
     for (int t = T - 1; t >= 0; t--) {
-      const int buf = t & 1;
-      if (t > 0) {
-        stage_C(t - 1, buf ^ 1);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      } else {
-        cp_async_wait_all();
-      }
-      const R* Cs = Cb + buf * NCS;
-      const R* cs = cb + buf * NZ;
-      // nominal point and state-dependent Jacobian entries
+      bwdp.acquire(t);
+      const R* Cs = bwdp.C(t);
+      const R* cs = bwdp.c(t);
+      // nominal point, state-dependent Jacobian entries
+      double xd[NX], ud[NU];
+      lds_row_d<NX>(Xn + t * XLD, xd);
+      lds_row_d<NU>(Un + t * ULD, ud);
       R xr[NX], ur[NU];
 #pragma unroll
-      for (int i = 0; i < NX; i++) xr[i] = (R)Xn[t * NX + i];
+      for (int i = 0; i < NX; i++) xr[i] = (R)xd[i];
 #pragma unroll
-      for (int i = 0; i < NU; i++) ur[i] = (R)Un[t * NU + i];
-      __syncwarp(gm);  // previous stage finished reading As/Bs/MA; staging visible
-      if constexpr (!M::kLinearParams) M::template jac_vary<R>(th_r, dt_r, xr, ur, As, LDA, Bs);
+      for (int i = 0; i < NU; i++) ur[i] = (R)ud[i];
+      __syncwarp(gm);  // previous stage done with As/Bs/MA; staging visible
+      if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
 #pragma unroll
       for (int i = 0; i < NZ; i++)
-        if ((i % G) == lane) zs[i] = (i < NX) ? xr[i < NX ? i : 0] : ur[i >= NX ? i - NX : 0];
+        if ((i % G) == lane) S.zs[i] = (i < NX) ? xr[i < NX ? i : 0] : ur[i >= NX ? i - NX : 0];
       __syncwarp(gm);
       // gz = C z + c ; qx = gz_x + A' Vx ; qu = gz_u + B' Vx   (kernels.py:395-410)
       R qx = R(0);
+      R zv[NZ], vx[NX];
+      lds_row<NZ>(S.zs, zv);
+      lds_row<NX>(S.Vx, vx);
       if (lane < NX) {
         const int a = lane;
         R s = cs[a];
         if constexpr (DIAG) {
-          s += Cs[a] * zs[a];
+          s += Cs[a] * S.zs[a];
         } else {
+          R crow[NZ];
+          lds_row<NZ>(Cs + a * ZLD, crow);
 #pragma unroll
-          for (int b = 0; b < NZ; b++) s += Cs[a * NZ + b] * zs[b];
+          for (int b = 0; b < NZ; b++) s += crow[b] * zv[b];
         }
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += As[b * LDA + a] * Vxs[b];
+        for (int b = 0; b < NX; b++) s += S.As[b * LDA + a] * vx[b];
         qx = s;
       }
       if (lane < NU) {
         const int a = lane;
         R s = cs[NX + a];
         if constexpr (DIAG) {
-          s += Cs[NX + a] * zs[NX + a];
+          s += Cs[NX + a] * S.zs[NX + a];
         } else {
+          R crow[NZ];
+          lds_row<NZ>(Cs + (NX + a) * ZLD, crow);
 #pragma unroll
-          for (int b = 0; b < NZ; b++) s += Cs[(NX + a) * NZ + b] * zs[b];
+          for (int b = 0; b < NZ; b++) s += crow[b] * zv[b];
         }
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += Bs[b * NU + a] * Vxs[b];
-        qus[a] = s;
+        for (int b = 0; b < NX; b++) s += S.Bs[b * LDB + a] * vx[b];
+        S.qu[a] = s;
       }
-      // MA = Vxx A, NB = Vxx B (row `lane`)
-      if (lane < NX) {
-        R ma[NX], nb[NU];
-#pragma unroll
-        for (int b = 0; b < NX; b++) ma[b] = R(0);
-#pragma unroll
-        for (int b = 0; b < NU; b++) nb[b] = R(0);
-#pragma unroll
-        for (int r = 0; r < NX; r++) {
-          const R v = vxx[r];
-#pragma unroll
-          for (int b = 0; b < NX; b++) ma[b] += v * As[r * LDA + b];
-#pragma unroll
-          for (int b = 0; b < NU; b++) nb[b] += v * Bs[r * NU + b];
-        }
-#pragma unroll
-        for (int b = 0; b < NX; b++) MA[lane * LDA + b] = ma[b];
-#pragma unroll
-        for (int b = 0; b < NU; b++) NB[lane * NU + b] = nb[b];
-      }
+      if (lane < NX) ric_MA_NB<M, DIAG, R>(S, lane, vxx);
       __syncwarp(gm);
-      // Quu = C_uu + B' NB (kernels.py:434-439)
-      for (int e = lane; e < NU * NU; e += G) {
-        const int i = e / NU, j = e % NU;
-        R s;
-        if constexpr (DIAG) {
-          s = (i == j) ? Cs[NX + i] : R(0);
-        } else {
-          s = Cs[(NX + i) * NZ + NX + j];
-        }
-#pragma unroll
-        for (int r = 0; r < NX; r++) s += Bs[r * NU + i] * NB[r * NU + j];
-        Quus[e] = s;
-      }
-      // Qux column `lane` (kernels.py:428-433) and Qxx row `lane` (kernels.py:422-427)
+      for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU);
       R quxc[NU], qxx[NX];
-      if (lane < NX) {
-        const int b = lane;
-#pragma unroll
-        for (int i = 0; i < NU; i++) {
-          R s;
-          if constexpr (DIAG) {
-            s = R(0);
-          } else {
-            s = Cs[(NX + i) * NZ + b];
-          }
-#pragma unroll
-          for (int r = 0; r < NX; r++) s += Bs[r * NU + i] * MA[r * LDA + b];
-          quxc[i] = s;
-        }
-        const int a = lane;
-#pragma unroll
-        for (int bb = 0; bb < NX; bb++) {
-          if constexpr (DIAG) {
-            qxx[bb] = (bb == a) ? Cs[a] : R(0);
-          } else {
-            qxx[bb] = Cs[a * NZ + bb];
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < NX; r++) {
-          const R ar = As[r * LDA + a];
-#pragma unroll
-          for (int bb = 0; bb < NX; bb++) qxx[bb] += ar * MA[r * LDA + bb];
-        }
-      }
+      if (lane < NX) ric_Qxx_Qux<M, DIAG, R>(S, Cs, lane, qxx, quxc);
       __syncwarp(gm);
-      // ---- stage QP on the control increment (double, all lanes redundantly) ----
-      double Quu_d[NU][NU], qu_d[NU], lo[NU], hi[NU], du[NU];
+      bwdp.release(t);  // C_t fully consumed: prefetch C_{t-1}
+      // ---- stage QP on the control increment (type R, all lanes redundantly) ----
+      R quu[NU][NU], qu_c[NU], lo[NU], hi[NU], du[NU];
       bool fr[NU];
-      Chol<NU> ch;
+      Chol<NU, R> ch;
 #pragma unroll
       for (int i = 0; i < NU; i++) {
-#pragma unroll
-        for (int j = 0; j < NU; j++) Quu_d[i][j] = (double)Quus[i * NU + j];
-        qu_d[i] = (double)qus[i];
-        const double un = Un[t * NU + i];
-        lo[i] = umin[i] - un;
-        hi[i] = umax[i] - un;
+        lds_row<NU>(S.Quu + i * LDB, quu[i]);
+        qu_c[i] = S.qu[i];
+        lo[i] = (R)(args.u_min[i] - ud[i]);
+        hi[i] = (R)(args.u_max[i] - ud[i]);
       }
-      const bool ok = stage_qp<NU>(Quu_d, qu_d, lo, hi, args.boxqp_max_iter, args.boxqp_tol, du, fr, ch);
+      const bool ok = stage_qp<NU, R>(quu, qu_c, lo, hi, args.boxqp_max_iter, (R)args.boxqp_tol, du, fr, ch);
       if (!ok) {
         fail_t = t;
         active = 0;
         break;
       }
       // k_t = du (all dims, kernels.py:478); K rows of free dims (kernels.py:481-489)
-      if (lane < NU) {
+      if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < NU; i++)
-          if (i == lane) kg[t * NU + i] = du[i];
+        for (int i = 0; i < NU; i++) kg[t * ULD + i] = (double)du[i];
       }
       R kcol[NU];
       if (lane < NX) {
         const int b = lane;
-        double rhs[NU], sol[NU];
+        R rhs[NU], sol[NU];
 #pragma unroll
-        for (int i = 0; i < NU; i++) rhs[i] = fr[i] ? (double)quxc[i] : 0.0;
-        chol_solve<NU>(ch, rhs, sol);
-#pragma unroll
-        for (int i = 0; i < NU; i++) {
-          kcol[i] = fr[i] ? (R)(-sol[i]) : R(0);
-          Kg[(t * NU + i) * NX + b] = kcol[i];
-          KT[b * NU + i] = kcol[i];
-          QuxT[b * NU + i] = quxc[i];
-        }
-        // (Quu K)[:, b] with the unregularised Quu (kernels.py:503-506)
+        for (int i = 0; i < NU; i++) rhs[i] = fr[i] ? quxc[i] : R(0);
+        chol_solve<NU, R>(ch, rhs, sol);
 #pragma unroll
         for (int i = 0; i < NU; i++) {
-          R s = R(0);
-#pragma unroll
-          for (int q = 0; q < NU; q++) s += Quus[i * NU + q] * kcol[q];
-          QuuKT[b * NU + i] = s;
+          kcol[i] = fr[i] ? -sol[i] : R(0);
+          Kg[(t * NU + i) * LDA + b] = kcol[i];
         }
-        // Vx update (kernels.py:491-498)
-        R kt[NU];
-#pragma unroll
-        for (int i = 0; i < NU; i++) kt[i] = (R)du[i];
+        ric_publish_cols<M, DIAG, R>(S, b, kcol, quxc, quu);
+        // Vx update (kernels.py:491-498), unregularised Quu
         R s = qx;
 #pragma unroll
         for (int r = 0; r < NU; r++) {
           R rowq = R(0);
 #pragma unroll
-          for (int q = 0; q < NU; q++) rowq += Quus[r * NU + q] * kt[q];
-          s += kcol[r] * (rowq + qus[r]) + quxc[r] * kt[r];
+          for (int q = 0; q < NU; q++) rowq += quu[r][q] * du[q];
+          s += kcol[r] * (rowq + qu_c[r]) + quxc[r] * du[r];
         }
-        Vxs[b] = s;  // all lanes finished reading Vx (qx/qu) before the last sync
+        S.Vx[b] = s;  // all lanes finished reading Vx (qx/qu) before the last sync
       }
       __syncwarp(gm);
-      // Vxx update row `lane` (kernels.py:499-507), then symmetrise (kernels.py:510-512)
-      if (lane < NX) {
-        const int a = lane;
-#pragma unroll
-        for (int bb = 0; bb < NX; bb++) {
-          R s = qxx[bb];
-#pragma unroll
-          for (int r = 0; r < NU; r++) {
-            const R Kra = kcol[r], Qra = quxc[r];
-            s += (Kra * QuuKT[bb * NU + r] + Kra * QuxT[bb * NU + r]) + Qra * KT[bb * NU + r];
-          }
-          MA[a * LDA + bb] = s;  // MA is dead after Qxx/Qux: reuse as the N buffer
-        }
-      }
+      if (lane < NX) ric_Vxx_row<M, DIAG, R>(S, lane, qxx, kcol, quxc);
       __syncwarp(gm);
-      if (lane < NX) {
-        const int a = lane;
-#pragma unroll
-        for (int bb = 0; bb < NX; bb++) vxx[bb] = R(0.5) * (MA[a * LDA + bb] + MA[bb * LDA + a]);
-      }
+      if (lane < NX) ric_symmetrize<M, DIAG, R>(S, lane, vxx);
     }
     cp_async_wait_all();
     __syncwarp(gm);
@@ -526,32 +411,28 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
         const int a_me = min(round * NSLOT + slot, NA - 1);
         const double alpha = args.alphas[a_me];
         double xc[NX];
-#pragma unroll
-        for (int i = 0; i < NX; i++) xc[i] = Xn[i];
+        lds_row_d<NX>(Xn, xc);
         double Jm = 0.0;
         bool dm = false;
-        stage_C(0, 0);
+        fwdp.start(0);
         for (int t = 0; t < T; t++) {
-          const int buf = t & 1;
-          if (t + 1 < T) {
-            stage_C(t + 1, buf ^ 1);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-          } else {
-            cp_async_wait_all();
-          }
+          fwdp.acquire(t);
           __syncwarp(gm);
           // feedback law u = clip(U + alpha k + K (x - X)) (kernels.py:560-568)
           constexpr int NUL = (NU + LC - 1) / LC;
+          double xbar[NX];
+          lds_row_d<NX>(Xn + t * XLD, xbar);
           double urr[NUL];
 #pragma unroll
           for (int rr = 0; rr < NUL; rr++) {
             const int r = j + rr * LC;
             double v = 0.0;
             if (r < NU) {
-              v = Un[t * NU + r] + alpha * kg[t * NU + r];
-              const R* Kr = Kg + (t * NU + r) * NX;
+              v = Un[t * ULD + r] + alpha * kg[t * ULD + r];
+              R krow[NX];
+              lds_row<NX>(Kg + (t * NU + r) * LDA, krow);
 #pragma unroll
-              for (int b = 0; b < NX; b++) v += (double)Kr[b] * (xc[b] - Xn[t * NX + b]);
+              for (int b = 0; b < NX; b++) v += (double)krow[b] * (xc[b] - xbar[b]);
               const double lo = args.u_min[r], hi = args.u_max[r];
               if (v < lo) v = lo;
               else if (v > hi) v = hi;
@@ -561,10 +442,12 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
           double u[NU];
 #pragma unroll
           for (int r = 0; r < NU; r++)
-            u[r] = __shfl_sync(smask, urr[r / LC], (lane & ~(LC - 1)) + (r % LC), G);
-          Jm += stage_cost(std::integral_constant<int, LC>{}, Cb + buf * NCS, cb + buf * NZ, xc, u, j, smask);
+            u[r] = (LC == 1) ? urr[r] : __shfl_sync(smask, urr[r / LC], (lane & ~(LC - 1)) + (r % LC), G);
+          Jm += stage_cost(std::integral_constant<int, LC>{}, fwdp.C(t), fwdp.c(t), xc, u, j, smask);
+          __syncwarp(gm);
+          fwdp.release(t);
           double xn[NX];
-          step_e<M, R>(th_e, dt_e, As, Bs, xc, u, xn);
+          step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
           bool fin = finite_(Jm);
 #pragma unroll
           for (int i = 0; i < NX; i++) {
@@ -616,16 +499,18 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
       // feedback at t has read the old nominal X_t.
       const double alpha = args.alphas[best];
       double xc[NX];
-#pragma unroll
-      for (int i = 0; i < NX; i++) xc[i] = Xn[i];
+      lds_row_d<NX>(Xn, xc);
       for (int t = 0; t < T; t++) {
         double v = 0.0;
         if (lane < NU) {
           const int r = lane;
-          v = Un[t * NU + r] + alpha * kg[t * NU + r];
-          const R* Kr = Kg + (t * NU + r) * NX;
+          double xbar[NX];
+          lds_row_d<NX>(Xn + t * XLD, xbar);
+          v = Un[t * ULD + r] + alpha * kg[t * ULD + r];
+          R krow[NX];
+          lds_row<NX>(Kg + (t * NU + r) * LDA, krow);
 #pragma unroll
-          for (int b = 0; b < NX; b++) v += (double)Kr[b] * (xc[b] - Xn[t * NX + b]);
+          for (int b = 0; b < NX; b++) v += (double)krow[b] * (xc[b] - xbar[b]);
           const double lo = args.u_min[r], hi = args.u_max[r];
           if (v < lo) v = lo;
           else if (v > hi) v = hi;
@@ -636,16 +521,16 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
         __syncwarp(gm);
 #pragma unroll
         for (int i = 0; i < NX; i++)
-          if ((i % G) == lane) Xn[t * NX + i] = xc[i];
-        if (lane < NU) Un[t * NU + lane] = v;
+          if ((i % G) == lane) Xn[t * XLD + i] = xc[i];
+        if (lane < NU) Un[t * ULD + lane] = v;
         double xn[NX];
-        step_e<M, R>(th_e, dt_e, As, Bs, xc, u, xn);
+        step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
 #pragma unroll
         for (int i = 0; i < NX; i++) xc[i] = xn[i];
       }
 #pragma unroll
       for (int i = 0; i < NX; i++)
-        if ((i % G) == lane) Xn[T * NX + i] = xc[i];
+        if ((i % G) == lane) Xn[T * XLD + i] = xc[i];
       __syncwarp(gm);
     }
     const double J_prev = J;
@@ -670,23 +555,24 @@ __global__ void __launch_bounds__(128) ilqr_forward_kernel(const FwdArgs args) {
   const bool failed = fail_t >= 0 || diverged;
   {
     R* Xo = (R*)args.X + (size_t)pid * (T + 1) * NX;
-    for (int e = lane; e < (T + 1) * NX; e += G) Xo[e] = (R)Xn[e];
+    for (int e = lane; e < (T + 1) * NX; e += G) Xo[e] = (R)Xn[(e / NX) * XLD + e % NX];
     R* Uo = (R*)args.U + (size_t)pid * T * NU;
-    for (int e = lane; e < T * NU; e += G) Uo[e] = (R)Un[e];
+    for (int e = lane; e < T * NU; e += G) Uo[e] = (R)Un[(e / NU) * ULD + e % NU];
     if (args.clamped) {
       uint8_t* co = args.clamped + (size_t)pid * T * NU;
       for (int e = lane; e < T * NU; e += G) {
         const int r = e % NU;
-        co[e] = (uint8_t)(Un[e] <= args.u_min[r] || Un[e] >= args.u_max[r]);
+        const double v = Un[(e / NU) * ULD + r];
+        co[e] = (uint8_t)(v <= args.u_min[r] || v >= args.u_max[r]);
       }
     }
     if (args.K) {
       R* Ko = (R*)args.K + (size_t)pid * T * NU * NX;
-      for (int e = lane; e < T * NU * NX; e += G) Ko[e] = Kg[e];
+      for (int e = lane; e < T * NU * NX; e += G) Ko[e] = Kg[(e / NX) * LDA + e % NX];
     }
     if (args.k) {
       R* ko = (R*)args.k + (size_t)pid * T * NU;
-      for (int e = lane; e < T * NU; e += G) ko[e] = (R)kg[e];
+      for (int e = lane; e < T * NU; e += G) ko[e] = (R)kg[(e / NU) * ULD + e % NU];
     }
     if (lane == 0) {
       ((R*)args.J)[pid] = (R)J;

@@ -132,19 +132,19 @@ __global__ void dynamics_kernel(int N, int stride, double dt, const R* theta, co
       for (int e = 0; e < NX * NU; e++) Bi[e] = th[NX * NX + e];
     }
   } else {
-    constexpr int NTHL = M::NTH > 0 ? M::NTH : 1;
-    R thr[NTHL];
+    R thr[M::NTH > 0 ? M::NTH : 1], P[M::NP];
 #pragma unroll
-    for (int a = 0; a < NTHL; a++) thr[a] = a < M::NTH ? th[a] : R(0);
+    for (int a = 0; a < M::NTH; a++) thr[a] = th[a];
+    M::template prep<R>(thr, P);
     if (xn) {
       R o[NX];
-      M::template step<R>(thr, (R)dt, xr, ur, o);
+      M::template step<R>(P, (R)dt, xr, ur, o);
 #pragma unroll
       for (int a = 0; a < NX; a++) xn[(size_t)i * NX + a] = o[a];
     }
     if (Ai && Bi) {
-      M::template jac_const<R>(thr, (R)dt, Ai, NX, Bi, 0, 1);
-      M::template jac_vary<R>(thr, (R)dt, xr, ur, Ai, NX, Bi);
+      M::template jac_const<R>(P, (R)dt, Ai, NX, Bi, NU, 0, 1);
+      M::template jac_vary<R>(P, (R)dt, xr, ur, Ai, NX, Bi, NU);
     }
   }
 }

@@ -14,9 +14,10 @@
 //   theta_grad(...)                    dL/dtheta contributions of one stage
 //                                      (SURVEY.md §8(a) NEW row)
 //
-// `th` points to the model parameters: a small register array for the quadrotors,
-// the smem copy of [A,B] for the linear model. Expression trees of the planar and
-// 13-state quadrotor steps follow oracle/diffmpc_oracle.c token for token.
+// `th` is the model's PREPARED parameter array (prep(): the raw parameters followed by
+// derived constants such as 1/m, 1/J, arm/sqrt(2)), so divisions by parameters become
+// multiplications (<= 1 ulp from the reference's divisions). Expression trees otherwise
+// follow oracle/diffmpc_oracle.c. The linear model keeps [A|B] in shared memory.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -31,8 +32,10 @@ constexpr double kInvSqrt2 = 0.7071067811865476;
 // ---------------------------------------------------------------------------
 template <int D>
 struct DoubleIntegrator {
-  static constexpr int NX = 2 * D, NU = D, NTH = 0, KIND = 0;
+  static constexpr int NX = 2 * D, NU = D, NTH = 0, NP = 1, KIND = 0;
   static constexpr bool kLinearParams = false;
+  template <class S>
+  DMPC_DEV static void prep(const S*, S* P) { P[0] = S(0); }
   template <class S>
   DMPC_DEV static void step(const S*, S dt, const S* x, const S* u, S* o) {
 #pragma unroll
@@ -42,18 +45,18 @@ struct DoubleIntegrator {
     }
   }
   template <class S>
-  DMPC_DEV static void jac_const(const S*, S dt, S* A, int lda, S* B, int lane, int G) {
+  DMPC_DEV static void jac_const(const S*, S dt, S* A, int lda, S* B, int ldb, int lane, int G) {
     for (int e = lane; e < NX * NX; e += G) {
       int i = e / NX, j = e % NX;
       A[i * lda + j] = (i == j) ? S(1) : ((i < D && j == i + D) ? dt : S(0));
     }
     for (int e = lane; e < NX * NU; e += G) {
       int i = e / NU, j = e % NU;
-      B[i * NU + j] = (i >= D && i - D == j) ? dt : S(0);
+      B[i * ldb + j] = (i >= D && i - D == j) ? dt : S(0);
     }
   }
   template <class S>
-  DMPC_DEV static void jac_vary(const S*, S, const S*, const S*, S*, int, S*) {}
+  DMPC_DEV static void jac_vary(const S*, S, const S*, const S*, S*, int, S*, int) {}
   template <class S>
   DMPC_DEV static void theta_grad(const S*, S, const S*, const S*, const S*, const S*, const S*,
                                   const S*, S*) {}
@@ -64,60 +67,68 @@ struct DoubleIntegrator {
 // th = [m, arm, I, g] (dynamics.py:57-70, kernels.py:52-65, 92-111)
 // ---------------------------------------------------------------------------
 struct PlanarQuad {
-  static constexpr int NX = 6, NU = 2, NTH = 4, KIND = 1;
+  static constexpr int NX = 6, NU = 2, NTH = 4, NP = 6, KIND = 1;
   static constexpr bool kLinearParams = false;
+  // P = [m, arm, I, g, 1/m, arm/I]
   template <class S>
-  DMPC_DEV static void step(const S* th, S dt, const S* x, const S* u, S* o) {
-    const S m = th[0], arm = th[1], inertia = th[2], g = th[3];
+  DMPC_DEV static void prep(const S* th, S* P) {
+    P[0] = th[0]; P[1] = th[1]; P[2] = th[2]; P[3] = th[3];
+    P[4] = S(1) / th[0];
+    P[5] = th[1] / th[2];
+  }
+  template <class S>
+  DMPC_DEV static void step(const S* P, S dt, const S* x, const S* u, S* o) {
+    const S g = P[3], im = P[4], aoi = P[5];
     S s, c;
     sincos_(x[2], &s, &c);
     const S thrust = u[0] + u[1];
     o[0] = x[0] + dt * x[3];
     o[1] = x[1] + dt * x[4];
     o[2] = x[2] + dt * x[5];
-    o[3] = x[3] + dt * (-thrust * s / m);
-    o[4] = x[4] + dt * (thrust * c / m - g);
-    o[5] = x[5] + dt * (arm * (u[1] - u[0]) / inertia);
+    o[3] = x[3] + dt * (-thrust * s * im);
+    o[4] = x[4] + dt * (thrust * c * im - g);
+    o[5] = x[5] + dt * ((u[1] - u[0]) * aoi);
   }
   template <class S>
-  DMPC_DEV static void jac_const(const S* th, S dt, S* A, int lda, S* B, int lane, int G) {
+  DMPC_DEV static void jac_const(const S* P, S dt, S* A, int lda, S* B, int ldb, int lane, int G) {
     for (int e = lane; e < NX * NX; e += G) {
       int i = e / NX, j = e % NX;
       A[i * lda + j] = (i == j) ? S(1) : ((i < 3 && j == i + 3) ? dt : S(0));
     }
-    for (int e = lane; e < NX * NU; e += G) B[e] = S(0);
+    for (int e = lane; e < NX * NU; e += G) B[(e / NU) * ldb + e % NU] = S(0);
     if (lane == 0) {
-      B[5 * 2 + 0] = -dt * th[1] / th[2];
-      B[5 * 2 + 1] = dt * th[1] / th[2];
+      B[5 * ldb + 0] = -dt * P[5];
+      B[5 * ldb + 1] = dt * P[5];
     }
   }
   template <class S>
-  DMPC_DEV static void jac_vary(const S* th, S dt, const S* x, const S* u, S* A, int lda, S* B) {
-    const S m = th[0];
+  DMPC_DEV static void jac_vary(const S* P, S dt, const S* x, const S* u, S* A, int lda, S* B, int ldb) {
+    const S im = P[4];
     S s, c;
     sincos_(x[2], &s, &c);
     const S thrust = u[0] + u[1];
-    A[3 * lda + 2] = -dt * thrust * c / m;
-    A[4 * lda + 2] = -dt * thrust * s / m;
-    B[3 * 2 + 0] = -dt * s / m;
-    B[3 * 2 + 1] = -dt * s / m;
-    B[4 * 2 + 0] = dt * c / m;
-    B[4 * 2 + 1] = dt * c / m;
+    const S dts = dt * s * im, dtc = dt * c * im;
+    A[3 * lda + 2] = -thrust * dtc;
+    A[4 * lda + 2] = -thrust * dts;
+    B[3 * ldb + 0] = -dts;
+    B[3 * ldb + 1] = -dts;
+    B[4 * ldb + 0] = dtc;
+    B[4 * ldb + 1] = dtc;
   }
   // g[p] += lh . df/dth_p + lam . (d2f/dth_p dz) dz   (oracle: theta_grad_stage)
   template <class S>
-  DMPC_DEV static void theta_grad(const S* th, S dt, const S* x, const S* u, const S* dx,
+  DMPC_DEV static void theta_grad(const S* P, S dt, const S* x, const S* u, const S* dx,
                                   const S* du, const S* lh, const S* lam, S* g) {
-    const S m = th[0], arm = th[1], I = th[2];
+    const S arm = P[1], I = P[2], im = P[4];
     S s, c;
     sincos_(x[2], &s, &c);
     const S F = u[0] + u[1], dF = du[0] + du[1], dd = u[1] - u[0], ddd = du[1] - du[0];
-    const S mm = m * m;
-    g[0] += lh[3] * (dt * F * s / mm) + lh[4] * (-dt * F * c / mm) +
-            lam[3] * (dt * (F * c * dx[2] + s * dF) / mm) +
-            lam[4] * (dt * (F * s * dx[2] - c * dF) / mm);
-    g[1] += lh[5] * (dt * dd / I) + lam[5] * (dt * ddd / I);
-    g[2] += lh[5] * (-dt * arm * dd / (I * I)) + lam[5] * (-dt * arm * ddd / (I * I));
+    const S im2 = dt * im * im;
+    const S iI = S(1) / I;
+    g[0] += lh[3] * (F * s * im2) + lh[4] * (-F * c * im2) +
+            lam[3] * ((F * c * dx[2] + s * dF) * im2) + lam[4] * ((F * s * dx[2] - c * dF) * im2);
+    g[1] += lh[5] * (dt * dd * iI) + lam[5] * (dt * ddd * iI);
+    g[2] += lh[5] * (-dt * arm * dd * iI * iI) + lam[5] * (-dt * arm * ddd * iI * iI);
     g[3] += lh[4] * (-dt);
   }
 
@@ -131,12 +142,26 @@ struct PlanarQuad {
 // th = [m, arm, Jx, Jy, Jz, kappa, g]. See paper_2605_29155_b200/dynamics.py.
 // ---------------------------------------------------------------------------
 struct Quad13 {
-  static constexpr int NX = 13, NU = 4, NTH = 7, KIND = 3;
+  static constexpr int NX = 13, NU = 4, NTH = 7, NP = 15, KIND = 3;
   static constexpr bool kLinearParams = false;
+  // P = [m, arm, Jx, Jy, Jz, kappa, g, 1/m, arm/sqrt2, 1/Jx, 1/Jy, 1/Jz, Jz-Jy, Jx-Jz, Jy-Jx]
   template <class S>
-  DMPC_DEV static void step(const S* th, S dt, const S* x, const S* u, S* o) {
-    const S m = th[0], l = th[1], Jx = th[2], Jy = th[3], Jz = th[4], kap = th[5], g = th[6];
-    const S d = l * S(kInvSqrt2);
+  DMPC_DEV static void prep(const S* th, S* P) {
+#pragma unroll
+    for (int i = 0; i < 7; i++) P[i] = th[i];
+    P[7] = S(1) / th[0];
+    P[8] = th[1] * S(kInvSqrt2);
+    P[9] = S(1) / th[2];
+    P[10] = S(1) / th[3];
+    P[11] = S(1) / th[4];
+    P[12] = th[4] - th[3];
+    P[13] = th[2] - th[4];
+    P[14] = th[3] - th[2];
+  }
+  template <class S>
+  DMPC_DEV static void step(const S* P, S dt, const S* x, const S* u, S* o) {
+    const S kap = P[5], g = P[6], im = P[7], d = P[8], iJx = P[9], iJy = P[10], iJz = P[11];
+    const S dzy = P[12], dxz = P[13], dyx = P[14];
     const S qw = x[3], qx = x[4], qy = x[5], qz = x[6];
     const S wx = x[10], wy = x[11], wz = x[12];
     const S F = ((u[0] + u[1]) + u[2]) + u[3];
@@ -147,7 +172,7 @@ struct Quad13 {
     const S r13 = S(2) * (qx * qz + qw * qy);
     const S r23 = S(2) * (qy * qz - qw * qx);
     const S r33 = S(1) - S(2) * (qx * qx + qy * qy);
-    const S a = F / m;
+    const S a = F * im;
     o[0] = x[0] + dt * x[7];
     o[1] = x[1] + dt * x[8];
     o[2] = x[2] + dt * x[9];
@@ -158,33 +183,33 @@ struct Quad13 {
     o[7] = x[7] + dt * (r13 * a);
     o[8] = x[8] + dt * (r23 * a);
     o[9] = x[9] + dt * (r33 * a - g);
-    o[10] = wx + dt * ((tx - (Jz - Jy) * wy * wz) / Jx);
-    o[11] = wy + dt * ((ty - (Jx - Jz) * wz * wx) / Jy);
-    o[12] = wz + dt * ((tz - (Jy - Jx) * wx * wy) / Jz);
+    o[10] = wx + dt * ((tx - dzy * wy * wz) * iJx);
+    o[11] = wy + dt * ((ty - dxz * wz * wx) * iJy);
+    o[12] = wz + dt * ((tz - dyx * wx * wy) * iJz);
   }
   template <class S>
-  DMPC_DEV static void jac_const(const S* th, S dt, S* A, int lda, S* B, int lane, int G) {
+  DMPC_DEV static void jac_const(const S* P, S dt, S* A, int lda, S* B, int ldb, int lane, int G) {
     for (int e = lane; e < NX * NX; e += G) {
       int i = e / NX, j = e % NX;
       A[i * lda + j] = (i == j) ? S(1) : ((i < 3 && j == i + 7) ? dt : S(0));
     }
-    for (int e = lane; e < NX * NU; e += G) B[e] = S(0);
+    for (int e = lane; e < NX * NU; e += G) B[(e / NU) * ldb + e % NU] = S(0);
     if (lane == 0) {
-      const S d = th[1] * S(kInvSqrt2);
-      const S bx = dt * d / th[2], by = dt * d / th[3], bz = dt * th[5] / th[4];
-      B[10 * 4 + 0] = bx;  B[10 * 4 + 1] = bx;  B[10 * 4 + 2] = -bx; B[10 * 4 + 3] = -bx;
-      B[11 * 4 + 0] = -by; B[11 * 4 + 1] = by;  B[11 * 4 + 2] = by;  B[11 * 4 + 3] = -by;
-      B[12 * 4 + 0] = bz;  B[12 * 4 + 1] = -bz; B[12 * 4 + 2] = bz;  B[12 * 4 + 3] = -bz;
+      const S bx = dt * P[8] * P[9], by = dt * P[8] * P[10], bz = dt * P[5] * P[11];
+      B[10 * ldb + 0] = bx;  B[10 * ldb + 1] = bx;  B[10 * ldb + 2] = -bx; B[10 * ldb + 3] = -bx;
+      B[11 * ldb + 0] = -by; B[11 * ldb + 1] = by;  B[11 * ldb + 2] = by;  B[11 * ldb + 3] = -by;
+      B[12 * ldb + 0] = bz;  B[12 * ldb + 1] = -bz; B[12 * ldb + 2] = bz;  B[12 * ldb + 3] = -bz;
     }
   }
   template <class S>
-  DMPC_DEV static void jac_vary(const S* th, S dt, const S* x, const S* u, S* A, int lda, S* B) {
-    const S m = th[0], Jx = th[2], Jy = th[3], Jz = th[4];
+  DMPC_DEV static void jac_vary(const S* P, S dt, const S* x, const S* u, S* A, int lda, S* B, int ldb) {
+    const S im = P[7], iJx = P[9], iJy = P[10], iJz = P[11];
+    const S dzy = P[12], dxz = P[13], dyx = P[14];
     const S qw = x[3], qx = x[4], qy = x[5], qz = x[6];
     const S wx = x[10], wy = x[11], wz = x[12];
     const S F = ((u[0] + u[1]) + u[2]) + u[3];
     const S hw = S(0.5) * dt;
-    const S a = F / m;
+    const S da = dt * (F * im);
     const S r13 = S(2) * (qx * qz + qw * qy);
     const S r23 = S(2) * (qy * qz - qw * qx);
     const S r33 = S(1) - S(2) * (qx * qx + qy * qy);
@@ -196,28 +221,29 @@ struct Quad13 {
     A[5 * lda + 10] = hw * qz; A[5 * lda + 11] = hw * qw; A[5 * lda + 12] = -hw * qx;
     A[6 * lda + 3] = hw * wz; A[6 * lda + 4] = hw * wy; A[6 * lda + 5] = -hw * wx;
     A[6 * lda + 10] = -hw * qy; A[6 * lda + 11] = hw * qx; A[6 * lda + 12] = hw * qw;
-    const S da = dt * a;
     A[7 * lda + 3] = da * (S(2) * qy); A[7 * lda + 4] = da * (S(2) * qz);
     A[7 * lda + 5] = da * (S(2) * qw); A[7 * lda + 6] = da * (S(2) * qx);
     A[8 * lda + 3] = da * (S(-2) * qx); A[8 * lda + 4] = da * (S(-2) * qw);
     A[8 * lda + 5] = da * (S(2) * qz); A[8 * lda + 6] = da * (S(2) * qy);
     A[9 * lda + 4] = da * (S(-4) * qx); A[9 * lda + 5] = da * (S(-4) * qy);
-    const S b7 = dt * r13 / m, b8 = dt * r23 / m, b9 = dt * r33 / m;
+    const S dm = dt * im;
+    const S b7 = r13 * dm, b8 = r23 * dm, b9 = r33 * dm;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      B[7 * 4 + j] = b7;
-      B[8 * 4 + j] = b8;
-      B[9 * 4 + j] = b9;
+      B[7 * ldb + j] = b7;
+      B[8 * ldb + j] = b8;
+      B[9 * ldb + j] = b9;
     }
-    A[10 * lda + 11] = -dt * ((Jz - Jy) * wz) / Jx; A[10 * lda + 12] = -dt * ((Jz - Jy) * wy) / Jx;
-    A[11 * lda + 10] = -dt * ((Jx - Jz) * wz) / Jy; A[11 * lda + 12] = -dt * ((Jx - Jz) * wx) / Jy;
-    A[12 * lda + 10] = -dt * ((Jy - Jx) * wy) / Jz; A[12 * lda + 11] = -dt * ((Jy - Jx) * wx) / Jz;
+    const S ex = -dt * iJx, ey = -dt * iJy, ez = -dt * iJz;
+    A[10 * lda + 11] = ex * (dzy * wz); A[10 * lda + 12] = ex * (dzy * wy);
+    A[11 * lda + 10] = ey * (dxz * wz); A[11 * lda + 12] = ey * (dxz * wx);
+    A[12 * lda + 10] = ez * (dyx * wy); A[12 * lda + 11] = ez * (dyx * wx);
   }
   template <class S>
-  DMPC_DEV static void theta_grad(const S* th, S dt, const S* x, const S* u, const S* dx,
+  DMPC_DEV static void theta_grad(const S* P, S dt, const S* x, const S* u, const S* dx,
                                   const S* du, const S* lh, const S* lam, S* g) {
-    const S m = th[0], l = th[1], Jx = th[2], Jy = th[3], Jz = th[4], kap = th[5];
-    const S d = l * S(kInvSqrt2);
+    const S kap = P[5], im = P[7], d = P[8], iJx = P[9], iJy = P[10], iJz = P[11];
+    const S dzy = P[12], dxz = P[13], dyx = P[14];
     const S qw = x[3], qx = x[4], qy = x[5], qz = x[6];
     const S wx = x[10], wy = x[11], wz = x[12];
     const S dqw = dx[3], dqx = dx[4], dqy = dx[5], dqz = dx[6];
@@ -233,30 +259,26 @@ struct Quad13 {
     const S dr13 = S(2) * (qy * dqw + qz * dqx + qw * dqy + qx * dqz);
     const S dr23 = S(2) * (-qx * dqw - qw * dqx + qz * dqy + qy * dqz);
     const S dr33 = S(-4) * (qx * dqx + qy * dqy);
-    const S im2 = dt / (m * m);
+    const S im2 = dt * im * im;
     g[0] += -im2 * F * (lh[7] * r13 + lh[8] * r23 + lh[9] * r33) -
             im2 * (lam[7] * (F * dr13 + r13 * dF) + lam[8] * (F * dr23 + r23 * dF) +
                    lam[9] * (F * dr33 + r33 * dF));
     const S c = S(kInvSqrt2);
-    g[1] += lh[10] * (dt * c * sx / Jx) + lh[11] * (dt * c * sy / Jy) +
-            lam[10] * (dt * c * dsx / Jx) + lam[11] * (dt * c * dsy / Jy);
-    const S e10 = tx - (Jz - Jy) * wy * wz, e11 = ty - (Jx - Jz) * wz * wx,
-            e12 = tz - (Jy - Jx) * wx * wy;
-    const S de10 = d * dsx - (Jz - Jy) * (wz * dwy + wy * dwz);
-    const S de11 = d * dsy - (Jx - Jz) * (wx * dwz + wz * dwx);
-    const S de12 = kap * dsz - (Jy - Jx) * (wy * dwx + wx * dwy);
+    g[1] += lh[10] * (dt * c * sx * iJx) + lh[11] * (dt * c * sy * iJy) +
+            lam[10] * (dt * c * dsx * iJx) + lam[11] * (dt * c * dsy * iJy);
+    const S e10 = tx - dzy * wy * wz, e11 = ty - dxz * wz * wx, e12 = tz - dyx * wx * wy;
+    const S de10 = d * dsx - dzy * (wz * dwy + wy * dwz);
+    const S de11 = d * dsy - dxz * (wx * dwz + wz * dwx);
+    const S de12 = kap * dsz - dyx * (wy * dwx + wx * dwy);
     const S pyz = wy * wz, pzx = wz * wx, pxy = wx * wy;
     const S dpyz = wz * dwy + wy * dwz, dpzx = wx * dwz + wz * dwx, dpxy = wy * dwx + wx * dwy;
-    g[2] += lh[10] * (-dt * e10 / (Jx * Jx)) + lh[11] * (-dt * pzx / Jy) + lh[12] * (dt * pxy / Jz) +
-            lam[10] * (-dt * de10 / (Jx * Jx)) + lam[11] * (-dt * dpzx / Jy) +
-            lam[12] * (dt * dpxy / Jz);
-    g[3] += lh[10] * (dt * pyz / Jx) + lh[11] * (-dt * e11 / (Jy * Jy)) + lh[12] * (-dt * pxy / Jz) +
-            lam[10] * (dt * dpyz / Jx) + lam[11] * (-dt * de11 / (Jy * Jy)) +
-            lam[12] * (-dt * dpxy / Jz);
-    g[4] += lh[10] * (-dt * pyz / Jx) + lh[11] * (dt * pzx / Jy) + lh[12] * (-dt * e12 / (Jz * Jz)) +
-            lam[10] * (-dt * dpyz / Jx) + lam[11] * (dt * dpzx / Jy) +
-            lam[12] * (-dt * de12 / (Jz * Jz));
-    g[5] += lh[12] * (dt * sz / Jz) + lam[12] * (dt * dsz / Jz);
+    g[2] += lh[10] * (-dt * e10 * iJx * iJx) + lh[11] * (-dt * pzx * iJy) + lh[12] * (dt * pxy * iJz) +
+            lam[10] * (-dt * de10 * iJx * iJx) + lam[11] * (-dt * dpzx * iJy) + lam[12] * (dt * dpxy * iJz);
+    g[3] += lh[10] * (dt * pyz * iJx) + lh[11] * (-dt * e11 * iJy * iJy) + lh[12] * (-dt * pxy * iJz) +
+            lam[10] * (dt * dpyz * iJx) + lam[11] * (-dt * de11 * iJy * iJy) + lam[12] * (-dt * dpxy * iJz);
+    g[4] += lh[10] * (-dt * pyz * iJx) + lh[11] * (dt * pzx * iJy) + lh[12] * (-dt * e12 * iJz * iJz) +
+            lam[10] * (-dt * dpyz * iJx) + lam[11] * (dt * dpzx * iJy) + lam[12] * (-dt * de12 * iJz * iJz);
+    g[5] += lh[12] * (dt * sz * iJz) + lam[12] * (dt * dsz * iJz);
     g[6] += lh[9] * (-dt);
   }
 };
@@ -268,7 +290,7 @@ struct Quad13 {
 // ---------------------------------------------------------------------------
 template <int NX_, int NU_>
 struct LinearModel {
-  static constexpr int NX = NX_, NU = NU_, NTH = NX_ * NX_ + NX_ * NU_, KIND = 2;
+  static constexpr int NX = NX_, NU = NU_, NTH = NX_ * NX_ + NX_ * NU_, NP = 1, KIND = 2;
   static constexpr bool kLinearParams = true;
 };
 

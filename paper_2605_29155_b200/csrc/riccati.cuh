@@ -1,0 +1,288 @@
+// riccati.cuh — shared-memory layout helpers and the lane-parallel Riccati building
+// blocks used by both the forward (iLQR) and backward (auxiliary LQR) kernels.
+//
+// Mapping: lane a < n_x of a problem's G-lane group owns ROW a of every n_x x n_x
+// quantity (V_xx, Q_xx, MA) and COLUMN a of every n_u x n_x quantity (Q_ux, K).
+// Operands every lane needs in full (A_t rows, MA rows, B_t rows, the K/Qux/QuuK
+// columns) live in shared memory with rows padded to 16 bytes, so each row is
+// fetched with 128-bit broadcast loads (LDS.128): the row-lane products issue one
+// vector load per 4 (f32) FMAs instead of one scalar load per FMA.
+#pragma once
+#include "common.cuh"
+
+namespace dmpc {
+
+template <class R>
+struct VecW {
+  static constexpr int N = 16 / (int)sizeof(R);
+};
+
+__host__ __device__ constexpr int rup(int v, int a) { return (v + a - 1) / a * a; }
+
+// Load the first N entries of a 16-byte aligned, padded smem row into registers.
+template <int N, class R>
+DMPC_DEV void lds_row(const R* __restrict__ p, R (&v)[N]) {
+  if constexpr (sizeof(R) == 4) {
+#pragma unroll
+    for (int q = 0; q < (N + 3) / 4; q++) {
+      const float4 t = reinterpret_cast<const float4*>(p)[q];
+      const float tt[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if (q * 4 + i < N) v[q * 4 + i] = tt[i];
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < (N + 1) / 2; q++) {
+      const double2 t = reinterpret_cast<const double2*>(p)[q];
+      const double tt[2] = {t.x, t.y};
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+        if (q * 2 + i < N) v[q * 2 + i] = tt[i];
+    }
+  }
+}
+
+template <int N>
+DMPC_DEV void lds_row_d(const double* __restrict__ p, double (&v)[N]) {
+#pragma unroll
+  for (int q = 0; q < (N + 1) / 2; q++) {
+    const double2 t = reinterpret_cast<const double2*>(p)[q];
+    v[2 * q] = t.x;
+    if (2 * q + 1 < N) v[2 * q + 1] = t.y;
+  }
+}
+
+// Padded leading dimensions (elements of R) for one model / precision.
+template <class M, bool DIAG, class R>
+struct Dims {
+  static constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
+  static constexpr int VN = VecW<R>::N;
+  static constexpr int LDA = rup(NX, VN);  // rows of A, MA, Vx
+  static constexpr int LDB = rup(NU, VN);  // rows of B, NB, K^T, Qux^T, (QuuK)^T, Quu
+  static constexpr int ZLD = rup(NZ, VN);  // z, c, rows of staged dense C
+  static constexpr int NCSP = DIAG ? ZLD : NZ * ZLD;  // staged C_t (padded rows)
+  static constexpr int NBUF = DIAG ? 2 : 1;            // staging buffers (dense: 1 to save smem)
+  static constexpr int NCS = DIAG ? NZ : NZ * NZ;     // C_t in global memory
+  static constexpr int XLD = rup(NX, 2);   // rows of the double trajectories
+  static constexpr int ULD = rup(NU, 2);
+};
+
+// Riccati scratch offsets (bytes), 16-byte aligned arrays.
+template <class M, bool DIAG, class R>
+struct RicLayout {
+  using D = Dims<M, DIAG, R>;
+  int oAs, oBs, oMA, oNB, oKT, oQuxT, oQuuKT, oQuu, oqu, oVx, ozs, oC, oc, end;
+  __host__ __device__ static RicLayout make(int o) {
+    RicLayout L;
+    const int s = (int)sizeof(R);
+    auto take = [&](int n) { int r = o; o = rup(o + n * s, 16); return r; };
+    L.oAs = take(D::NX * D::LDA);
+    L.oBs = take(D::NX * D::LDB);
+    L.oMA = take(D::NX * D::LDA);
+    L.oNB = take(D::NX * D::LDB);
+    L.oKT = take(D::NX * D::LDB);
+    L.oQuxT = take(D::NX * D::LDB);
+    L.oQuuKT = take(D::NX * D::LDB);
+    L.oQuu = take(D::NU * D::LDB);
+    L.oqu = take(D::LDB);
+    L.oVx = take(D::LDA);
+    L.ozs = take(D::ZLD);
+    L.oC = take(D::NBUF * D::NCSP);
+    L.oc = take(D::NBUF * D::ZLD);
+    L.end = o;
+    return L;
+  }
+};
+
+template <class M, bool DIAG, class R>
+struct Ric {
+  using D = Dims<M, DIAG, R>;
+  R *As, *Bs, *MA, *NB, *KT, *QuxT, *QuuKT, *Quu, *qu, *Vx, *zs, *Cb, *cb;
+  DMPC_DEV void bind(unsigned char* base, const RicLayout<M, DIAG, R>& L) {
+    As = (R*)(base + L.oAs); Bs = (R*)(base + L.oBs); MA = (R*)(base + L.oMA);
+    NB = (R*)(base + L.oNB); KT = (R*)(base + L.oKT); QuxT = (R*)(base + L.oQuxT);
+    QuuKT = (R*)(base + L.oQuuKT); Quu = (R*)(base + L.oQuu); qu = (R*)(base + L.oqu);
+    Vx = (R*)(base + L.oVx); zs = (R*)(base + L.ozs); Cb = (R*)(base + L.oC); cb = (R*)(base + L.oc);
+  }
+};
+
+// cp.async C_t (and c_t) into staging buffer `buf`, remapping rows to the padded stride.
+template <class M, bool DIAG, class R, int G>
+DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, int t, int buf, int lane) {
+  using D = Dims<M, DIAG, R>;
+  const R* src = Cg + (size_t)t * D::NCS;
+  R* dst = S.Cb + buf * D::NCSP;
+  if constexpr (DIAG) {
+    for (int e = lane; e < D::NZ; e += G) cp_async_elem(dst + e, src + e);
+  } else {
+    for (int e = lane; e < D::NCS; e += G) cp_async_elem(dst + (e / D::NZ) * D::ZLD + e % D::NZ, src + e);
+  }
+  if (cg) {
+    const R* s2 = cg + (size_t)t * D::NZ;
+    R* d2 = S.cb + buf * D::ZLD;
+    for (int e = lane; e < D::NZ; e += G) cp_async_elem(d2 + e, s2 + e);
+  }
+  cp_async_commit();
+}
+
+// Software pipeline over the per-stage cost tensors: `acquire(t)` makes C_t resident
+// (issuing the prefetch of the next stage first when double-buffered); `release(t)`
+// is called once every lane is done with C_t and, when single-buffered, issues the
+// prefetch of the next stage into the same buffer. `step` is the traversal
+// direction (-1 backward sweeps, +1 forward rollouts).
+template <class M, bool DIAG, class R, int G>
+struct CostPipe {
+  using D = Dims<M, DIAG, R>;
+  const Ric<M, DIAG, R>* S;
+  const R* Cg;
+  const R* cg;
+  int T, lane, step;
+  DMPC_DEV int buf(int t) const { return D::NBUF == 2 ? (t & 1) : 0; }
+  DMPC_DEV void start(int t0) { stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, t0, buf(t0), lane); }
+  DMPC_DEV void acquire(int t) {
+    const int tn = t + step;
+    if (D::NBUF == 2 && tn >= 0 && tn < T) {
+      stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, tn, buf(tn), lane);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      cp_async_wait_all();
+    }
+  }
+  DMPC_DEV void release(int t) {
+    const int tn = t + step;
+    if (D::NBUF == 1 && tn >= 0 && tn < T) stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, tn, 0, lane);
+  }
+  DMPC_DEV const R* C(int t) const { return S->Cb + buf(t) * D::NCSP; }
+  DMPC_DEV const R* c(int t) const { return S->cb + buf(t) * D::ZLD; }
+};
+
+// ---------------------------------------------------------------------------
+// MA = V_xx A, NB = V_xx B (row `a` from the lane's register row of V_xx)
+// (kernels.py:411-421 / 629-639)
+// ---------------------------------------------------------------------------
+template <class M, bool DIAG, class R>
+DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int a, const R (&vxx)[M::NX]) {
+  using D = Dims<M, DIAG, R>;
+  constexpr int NX = M::NX, NU = M::NU;
+  R ma[NX], nb[NU];
+#pragma unroll
+  for (int b = 0; b < NX; b++) ma[b] = R(0);
+#pragma unroll
+  for (int b = 0; b < NU; b++) nb[b] = R(0);
+#pragma unroll
+  for (int r = 0; r < NX; r++) {
+    R arow[NX], brow[NU];
+    lds_row<NX>(S.As + r * D::LDA, arow);
+    lds_row<NU>(S.Bs + r * D::LDB, brow);
+    const R v = vxx[r];
+#pragma unroll
+    for (int b = 0; b < NX; b++) ma[b] += v * arow[b];
+#pragma unroll
+    for (int b = 0; b < NU; b++) nb[b] += v * brow[b];
+  }
+#pragma unroll
+  for (int b = 0; b < NX; b++) S.MA[a * D::LDA + b] = ma[b];
+#pragma unroll
+  for (int b = 0; b < NU; b++) S.NB[a * D::LDB + b] = nb[b];
+}
+
+// Q_xx row a = C_xx[a,:] + sum_r A[r,a] MA[r,:]  (kernels.py:422-427), and
+// Q_ux column a = C_ux[:,a] + sum_r B[r,:] MA[r,a] (kernels.py:428-433).
+template <class M, bool DIAG, class R>
+DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int a, R (&qxx)[M::NX], R (&quxc)[M::NU]) {
+  using D = Dims<M, DIAG, R>;
+  constexpr int NX = M::NX, NU = M::NU;
+  if constexpr (DIAG) {
+#pragma unroll
+    for (int bb = 0; bb < NX; bb++) qxx[bb] = R(0);
+    const R caa = Cs[a];
+#pragma unroll
+    for (int bb = 0; bb < NX; bb++)
+      if (bb == a) qxx[bb] = caa;
+#pragma unroll
+    for (int i = 0; i < NU; i++) quxc[i] = R(0);
+  } else {
+    lds_row<NX>(Cs + a * D::ZLD, qxx);
+#pragma unroll
+    for (int i = 0; i < NU; i++) quxc[i] = Cs[(NX + i) * D::ZLD + a];
+  }
+#pragma unroll
+  for (int r = 0; r < NX; r++) {
+    R mrow[NX], brow[NU];
+    lds_row<NX>(S.MA + r * D::LDA, mrow);
+    lds_row<NU>(S.Bs + r * D::LDB, brow);
+    const R ar = S.As[r * D::LDA + a];
+    const R mra = S.MA[r * D::LDA + a];
+#pragma unroll
+    for (int bb = 0; bb < NX; bb++) qxx[bb] += ar * mrow[bb];
+#pragma unroll
+    for (int i = 0; i < NU; i++) quxc[i] += brow[i] * mra;
+  }
+}
+
+// Q_uu entry (i,j) = C_uu[i,j] + sum_r B[r,i] NB[r,j]  (kernels.py:434-439)
+template <class M, bool DIAG, class R>
+DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j) {
+  using D = Dims<M, DIAG, R>;
+  constexpr int NX = M::NX;
+  R s;
+  if constexpr (DIAG) {
+    s = (i == j) ? Cs[NX + i] : R(0);
+  } else {
+    s = Cs[(NX + i) * D::ZLD + NX + j];
+  }
+#pragma unroll
+  for (int r = 0; r < NX; r++) s += S.Bs[r * D::LDB + i] * S.NB[r * D::LDB + j];
+  return s;
+}
+
+// After the gains: publish column a of K, Qux, Quu K; return nothing. The value
+// Hessian update then reads those columns for every b (kernels.py:499-507).
+template <class M, bool DIAG, class R>
+DMPC_DEV void ric_publish_cols(const Ric<M, DIAG, R>& S, int a, const R (&kcol)[M::NU], const R (&quxc)[M::NU],
+                               const R (&quu)[M::NU][M::NU]) {
+  using D = Dims<M, DIAG, R>;
+  constexpr int NU = M::NU;
+#pragma unroll
+  for (int i = 0; i < NU; i++) {
+    S.KT[a * D::LDB + i] = kcol[i];
+    S.QuxT[a * D::LDB + i] = quxc[i];
+    R s = R(0);
+#pragma unroll
+    for (int q = 0; q < NU; q++) s += quu[i][q] * kcol[q];
+    S.QuuKT[a * D::LDB + i] = s;
+  }
+}
+
+// newVxx row a -> N (aliases MA). s = Qxx[a,b] + sum_r (K_ra QuuK_rb + K_ra Qux_rb) + Qux_ra K_rb
+template <class M, bool DIAG, class R>
+DMPC_DEV void ric_Vxx_row(const Ric<M, DIAG, R>& S, int a, const R (&qxx)[M::NX], const R (&kcol)[M::NU],
+                          const R (&quxc)[M::NU]) {
+  using D = Dims<M, DIAG, R>;
+  constexpr int NX = M::NX, NU = M::NU;
+#pragma unroll
+  for (int bb = 0; bb < NX; bb++) {
+    R kq[NU], qx[NU], kk[NU];
+    lds_row<NU>(S.QuuKT + bb * D::LDB, kq);
+    lds_row<NU>(S.QuxT + bb * D::LDB, qx);
+    lds_row<NU>(S.KT + bb * D::LDB, kk);
+    R s = qxx[bb];
+#pragma unroll
+    for (int r = 0; r < NU; r++) s += (kcol[r] * kq[r] + kcol[r] * qx[r]) + quxc[r] * kk[r];
+    S.MA[a * D::LDA + bb] = s;
+  }
+}
+
+// V_xx row a = (N[a,:] + N[:,a]) / 2  (kernels.py:510-512)
+template <class M, bool DIAG, class R>
+DMPC_DEV void ric_symmetrize(const Ric<M, DIAG, R>& S, int a, R (&vxx)[M::NX]) {
+  using D = Dims<M, DIAG, R>;
+  constexpr int NX = M::NX;
+  R row[NX];
+  lds_row<NX>(S.MA + a * D::LDA, row);
+#pragma unroll
+  for (int bb = 0; bb < NX; bb++) vxx[bb] = R(0.5) * (row[bb] + S.MA[bb * D::LDA + a]);
+}
+
+}  // namespace dmpc
