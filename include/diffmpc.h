@@ -153,6 +153,9 @@ int64_t diffmpc_launch_count(void);
 /* Message for the last configuration error on this thread. */
 const char* diffmpc_last_error(void);
 int32_t diffmpc_abi_version(void);
+/* Measurement utility: FP32 FFMA throughput probe, blocks x 256 threads x iters x 128 FMAs
+ * (the roofline denominator for the FP32 CUDA-core kernels). */
+int diffmpc_probe_ffma(int blocks, int iters, void* out, void* stream);
 
 #ifdef __cplusplus
 }

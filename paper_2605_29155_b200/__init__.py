@@ -11,6 +11,7 @@ Heavy modules (torch, the CUDA library) are imported lazily.
 from .errors import ConfigError, DivergenceError, ExtensionMissingError, NumericError
 from .dynamics import DynModel
 from .settings import SolveSettings, DEFAULT_ALPHAS
+from . import _abi, problems, roofline  # noqa: F401  (host-only modules)
 
 __all__ = [
     "ConfigError", "DivergenceError", "NumericError", "ExtensionMissingError",
@@ -21,7 +22,7 @@ __all__ = [
 
 
 def __getattr__(name):
-    if name in ("StageCostParams", "Trajectory", "stage_cost", "total_cost"):
+    if name in ("StageCostParams", "Trajectory"):
         from . import qcost
         return getattr(qcost, name)
     if name in ("solve_raw", "solve_diag", "backward_raw", "SolveOutput", "GradOutput"):

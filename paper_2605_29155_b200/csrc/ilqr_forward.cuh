@@ -357,10 +357,18 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
         active = 0;
         break;
       }
-      // k_t = du (all dims, kernels.py:478); K rows of free dims (kernels.py:481-489)
+      // k_t = du (all dims, kernels.py:478); K rows of free dims (kernels.py:481-489).
+      // A coordinate the QP left on a bound is stored as the double-precision bound
+      // offset (u_min - U_t or u_max - U_t), exactly the value the reference's boxQP
+      // clamps to, so U_t + k_t lands on the bound bit-exactly (clamp masks match).
       if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < NU; i++) kg[t * ULD + i] = (double)du[i];
+        for (int i = 0; i < NU; i++) {
+          double kd = (double)du[i];
+          if (du[i] <= lo[i]) kd = args.u_min[i] - ud[i];
+          else if (du[i] >= hi[i]) kd = args.u_max[i] - ud[i];
+          kg[t * ULD + i] = kd;
+        }
       }
       R kcol[NU];
       if (lane < NX) {
