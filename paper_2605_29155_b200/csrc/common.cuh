@@ -44,6 +44,9 @@ DMPC_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: 
 template <class T>
 DMPC_DEV bool finite_(T v) { return isfinite(v); }
 
+DMPC_DEV float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+DMPC_DEV double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
 // ---------------------------------------------------------------------------
 // Stage QP control block (kernels.py:195-318 boxqp_one/_chol_* and the lambda
 // schedule of backward_range, kernels.py:444-489), in double, executed redundantly

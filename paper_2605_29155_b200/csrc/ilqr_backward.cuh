@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
           for (int e = lane; e < NZ * NZ; e += G) {
             const int a = e / NZ, b = e % NZ;
             const R za = zat(a), zb = zat(b);
-            const R v = (clat(a) || clat(b)) ? R(0) : R(0.5) * (dzat(a) * zb + za * dzat(b));
+            // products rounded separately (no FMA contraction) so dC is exactly symmetric
+            const R v = (clat(a) || clat(b)) ? R(0) : R(0.5) * (mul_rn(dzat(a), zb) + mul_rn(za, dzat(b)));
             dCo[(size_t)t * NZ * NZ + e] = v + R(0.5) * sJ * za * zb;
           }
         }

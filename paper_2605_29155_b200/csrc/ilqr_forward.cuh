@@ -167,8 +167,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
   // ---- load x0, U_warm (clipped, ilqr.py:165); zero K, k (Workspace init) ----
   {
     const R* xg = (const R*)args.x0 + (size_t)pid * NX;
+    #pragma unroll 1
     for (int e = lane; e < NX; e += G) Xn[e] = (double)xg[e];
     const R* ug = (const R*)args.U_warm + (size_t)pid * T * NU;
+    #pragma unroll 1
     for (int e = lane; e < T * NU; e += G) {
       double v = (double)ug[e];
       const int t = e / NU, r = e % NU;
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
       Un[t * ULD + r] = v;
       kg[t * ULD + r] = 0.0;
     }
+    #pragma unroll 1
     for (int e = lane; e < T * NU * LDA; e += G) Kg[e] = R(0);
   }
   __syncwarp(gm);
@@ -563,11 +566,14 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
   const bool failed = fail_t >= 0 || diverged;
   {
     R* Xo = (R*)args.X + (size_t)pid * (T + 1) * NX;
+    #pragma unroll 1
     for (int e = lane; e < (T + 1) * NX; e += G) Xo[e] = (R)Xn[(e / NX) * XLD + e % NX];
     R* Uo = (R*)args.U + (size_t)pid * T * NU;
+    #pragma unroll 1
     for (int e = lane; e < T * NU; e += G) Uo[e] = (R)Un[(e / NU) * ULD + e % NU];
     if (args.clamped) {
       uint8_t* co = args.clamped + (size_t)pid * T * NU;
+      #pragma unroll 1
       for (int e = lane; e < T * NU; e += G) {
         const int r = e % NU;
         const double v = Un[(e / NU) * ULD + r];
@@ -576,10 +582,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
     }
     if (args.K) {
       R* Ko = (R*)args.K + (size_t)pid * T * NU * NX;
+      #pragma unroll 1
       for (int e = lane; e < T * NU * NX; e += G) Ko[e] = Kg[(e / NX) * LDA + e % NX];
     }
     if (args.k) {
       R* ko = (R*)args.k + (size_t)pid * T * NU;
+      #pragma unroll 1
       for (int e = lane; e < T * NU; e += G) ko[e] = (R)kg[(e / NU) * ULD + e % NU];
     }
     if (lane == 0) {

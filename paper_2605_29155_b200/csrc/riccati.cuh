@@ -116,7 +116,24 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
   if constexpr (DIAG) {
     for (int e = lane; e < D::NZ; e += G) cp_async_elem(dst + e, src + e);
   } else {
-    for (int e = lane; e < D::NCS; e += G) cp_async_elem(dst + (e / D::NZ) * D::ZLD + e % D::NZ, src + e);
+    // element e -> padded (row, col); advanced incrementally (no div/mod per element)
+    int col = lane % D::NZ, off = (lane / D::NZ) * D::ZLD + col;
+#pragma unroll 4
+    for (int e = lane; e < D::NCS; e += G) {
+      cp_async_elem(dst + off, src + e);
+      col += G;
+      off += G;
+      if constexpr (G <= D::NZ) {  // at most one wrap: branch-free select
+        const bool wrap = col >= D::NZ;
+        col = wrap ? col - D::NZ : col;
+        off = wrap ? off + (D::ZLD - D::NZ) : off;
+      } else {
+        while (col >= D::NZ) {
+          col -= D::NZ;
+          off += D::ZLD - D::NZ;
+        }
+      }
+    }
   }
   if (cg) {
     const R* s2 = cg + (size_t)t * D::NZ;
