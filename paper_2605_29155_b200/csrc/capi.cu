@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -38,6 +39,15 @@ int fail(const char* fmt, ...) {
   va_end(ap);
   g_last_error = buf;
   return -1;
+}
+
+int group_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DIFFMPC_GROUP");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 int max_smem_optin() {

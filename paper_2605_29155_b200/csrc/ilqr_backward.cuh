@@ -65,10 +65,11 @@ struct BwdLayout {
 };
 
 template <class M, int G, bool DIAG, class R>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2) ilqr_backward_kernel(const BwdArgs args) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : 3)) : 2) ilqr_backward_kernel(const BwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD;
+  constexpr int RPL = (NX + G - 1) / G;  // state rows owned by each lane
   using Lay = BwdLayout<M, DIAG, R>;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -146,9 +147,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
   // ======================= auxiliary Riccati sweep (kernels.py:582-707) =========
   int fail_t = -1;
   {
-    R vxx[NX];
+    R vxx[RPL][NX];
 #pragma unroll
-    for (int b = 0; b < NX; b++) vxx[b] = R(0);
+    for (int k = 0; k < RPL; k++)
+#pragma unroll
+      for (int bb = 0; bb < NX; bb++) vxx[k][bb] = R(0);
     ricp.start(T - 1);
     for (int t = T - 1; t >= 0; t--) {
       ricp.acquire(t);
@@ -159,28 +162,28 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
       __syncwarp(gm);
       if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
       __syncwarp(gm);
-      R qx = R(0);
+      R qx[RPL];
       R vx[NX];
       lds_row<NX>(S.Vx, vx);
-      if (lane < NX) {
-        const int a = lane;
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int a = min(row_of<G, RPL>(lane, k), NX - 1);
         R s = sXg ? sXg[t * NX + a] : R(0);
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += S.As[b * LDA + a] * vx[b];
-        qx = s;
+        for (int b2 = 0; b2 < NX; b2++) s += S.As[b2 * LDA + a] * vx[b2];
+        qx[k] = s;
       }
-      if (lane < NU) {
-        const int a = lane;
+      for (int a = lane; a < NU; a += G) {
         R s = sUg ? sUg[t * NU + a] : R(0);
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += S.Bs[b * LDB + a] * vx[b];
+        for (int b2 = 0; b2 < NX; b2++) s += S.Bs[b2 * LDB + a] * vx[b2];
         S.qu[a] = s;
       }
-      if (lane < NX) ric_MA_NB<M, DIAG, R>(S, lane, vxx);
+      ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx);
       __syncwarp(gm);
       for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU);
-      R quxc[NU], qxx[NX];
-      if (lane < NX) ric_Qxx_Qux<M, DIAG, R>(S, Cs, lane, qxx, quxc);
+      R quxc[RPL][NU], qxx[RPL][NX];
+      ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc);
       __syncwarp(gm);
       ricp.release(t);
       // freeze clamped dimensions (kernels.py:658-667)
@@ -188,10 +191,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
       bool clm[NU];
 #pragma unroll
       for (int i = 0; i < NU; i++) {
-        R qrow[NU];
-        lds_row<NU>(S.Quu + i * LDB, qrow);
-#pragma unroll
-        for (int j = 0; j < NU; j++) quu[i][j] = qrow[j];
+        lds_row<NU>(S.Quu + i * LDB, quu[i]);
         qu[i] = S.qu[i];
         clm[i] = cl[t * NU + i] != 0;
       }
@@ -199,11 +199,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
       for (int a = 0; a < NU; a++) {
         if (clm[a]) {
           qu[a] = R(0);
-          quxc[a] = R(0);
 #pragma unroll
-          for (int b = 0; b < NU; b++) {
-            quu[a][b] = R(0);
-            quu[b][a] = R(0);
+          for (int k = 0; k < RPL; k++) quxc[k][a] = R(0);
+#pragma unroll
+          for (int b2 = 0; b2 < NU; b2++) {
+            quu[a][b2] = R(0);
+            quu[b2][a] = R(0);
           }
           quu[a][a] = R(1);
         }
@@ -228,31 +229,33 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
 #pragma unroll
         for (int i = 0; i < NU; i++) ka[t * LDB + i] = kt[i];
       }
-      R kcol[NU];
-      if (lane < NX) {
-        const int b = lane;
+      R kcol[RPL][NU];
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int b2 = row_of<G, RPL>(lane, k);
         R sol[NU];
-        chol_solve<NU, R>(ch, quxc, sol);
+        chol_solve<NU, R>(ch, quxc[k], sol);
 #pragma unroll
-        for (int i = 0; i < NU; i++) {
-          kcol[i] = -sol[i];
-          Ka[(t * NU + i) * LDA + b] = kcol[i];
+        for (int i = 0; i < NU; i++) kcol[k][i] = -sol[i];
+        if (b2 < NX) {
+#pragma unroll
+          for (int i = 0; i < NU; i++) Ka[(t * NU + i) * LDA + b2] = kcol[k][i];
+          ric_publish_cols<M, DIAG, R>(S, b2, kcol[k], quxc[k], quu);
+          R s = qx[k];
+#pragma unroll
+          for (int r = 0; r < NU; r++) {
+            R rowq = R(0);
+#pragma unroll
+            for (int q = 0; q < NU; q++) rowq += quu[r][q] * kt[q];
+            s += kcol[k][r] * (rowq + qu[r]) + quxc[k][r] * kt[r];
+          }
+          S.Vx[b2] = s;
         }
-        ric_publish_cols<M, DIAG, R>(S, b, kcol, quxc, quu);
-        R s = qx;
-#pragma unroll
-        for (int r = 0; r < NU; r++) {
-          R rowq = R(0);
-#pragma unroll
-          for (int q = 0; q < NU; q++) rowq += quu[r][q] * kt[q];
-          s += kcol[r] * (rowq + qu[r]) + quxc[r] * kt[r];
-        }
-        S.Vx[b] = s;
       }
       __syncwarp(gm);
-      if (lane < NX) ric_Vxx_row<M, DIAG, R>(S, lane, qxx, kcol, quxc);
+      ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc);
       __syncwarp(gm);
-      if (lane < NX) ric_symmetrize<M, DIAG, R>(S, lane, vxx);
+      ric_symmetrize<M, DIAG, R, G, RPL>(S, lane, vxx);
     }
     cp_async_wait_all();
     __syncwarp(gm);
@@ -280,8 +283,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
       if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
       R dx[NX];
       lds_row<NX>(dXs + t * LDA, dx);
-      if (lane < NU) {
-        const int r = lane;
+      for (int r = lane; r < NU; r += G) {
         R s = ka[t * LDB + r];
         R krow[NX];
         lds_row<NX>(Ka + (t * NU + r) * LDA, krow);
@@ -292,17 +294,20 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
       __syncwarp(gm);
       R du[NU];
       lds_row<NU>(dUs + t * LDB, du);
-      if (lane < NX) {
-        const int a = lane;
-        R arow[NX], brow[NU];
-        lds_row<NX>(S.As + a * LDA, arow);
-        lds_row<NU>(S.Bs + a * LDB, brow);
-        R s = R(0);
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += arow[b] * dx[b];
+      for (int k = 0; k < RPL; k++) {
+        const int a = row_of<G, RPL>(lane, k);
+        if (a < NX) {
+          R arow[NX], brow[NU];
+          lds_row<NX>(S.As + a * LDA, arow);
+          lds_row<NU>(S.Bs + a * LDB, brow);
+          R s = R(0);
 #pragma unroll
-        for (int b = 0; b < NU; b++) s += brow[b] * du[b];
-        dXs[(t + 1) * LDA + a] = s;
+          for (int b = 0; b < NX; b++) s += arow[b] * dx[b];
+#pragma unroll
+          for (int b = 0; b < NU; b++) s += brow[b] * du[b];
+          dXs[(t + 1) * LDA + a] = s;
+        }
       }
       // assembly of stage t: dc = dz, dC = 0.5 (dz z' + z dz'), clamped rows/cols zero;
       // plus the optimal-cost terms sJ z and sJ/2 z z'
@@ -337,9 +342,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
 #pragma unroll
     for (int i = 0; i < (M::NTH > 0 && !M::kLinearParams ? M::NTH : 1); i++) gth[i] = R(0);
     constexpr int NZL = M::kLinearParams ? NZ : 1;
-    R grow[NZL];  // linear model: row `lane` of [dA | dB]
+    R grow[RPL][NZL];  // linear model: the lane's rows of [dA | dB]
 #pragma unroll
-    for (int i = 0; i < NZL; i++) grow[i] = R(0);
+    for (int k = 0; k < RPL; k++)
+#pragma unroll
+      for (int i = 0; i < NZL; i++) grow[k][i] = R(0);
     if (want_adjoint) {
       for (int e = lane; e < NX; e += G) {
         lams[e] = R(0);
@@ -360,13 +367,14 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
         __syncwarp(gm);
         if (want_theta) {
           if constexpr (M::kLinearParams) {
-            if (lane < NX) {
-              const int i = lane;
+#pragma unroll
+            for (int k = 0; k < RPL; k++) {
+              const int i = min(row_of<G, RPL>(lane, k), NX - 1);
               const R lhi = lhs[i], lmi = lams[i], lsi = sJ * lams[i];
 #pragma unroll
-              for (int j2 = 0; j2 < NX; j2++) grow[j2] += lhi * xr[j2] + lmi * dx[j2] + lsi * xr[j2];
+              for (int j2 = 0; j2 < NX; j2++) grow[k][j2] += lhi * xr[j2] + lmi * dx[j2] + lsi * xr[j2];
 #pragma unroll
-              for (int j2 = 0; j2 < NU; j2++) grow[NX + j2] += lhi * ur[j2] + lmi * du[j2] + lsi * ur[j2];
+              for (int j2 = 0; j2 < NU; j2++) grow[k][NX + j2] += lhi * ur[j2] + lmi * du[j2] + lsi * ur[j2];
             }
           } else if constexpr (M::NTH > 0) {
             R lhe[NX];
@@ -377,9 +385,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
         }
         const R* Cs = adjp.C(t);
         const R* cs = adjp.c(t);
-        R nl = R(0), nh = R(0);
-        if (lane < NX) {
-          const int a = lane;
+        R nl[RPL], nh[RPL];
+#pragma unroll
+        for (int k = 0; k < RPL; k++) {
+          const int a = min(row_of<G, RPL>(lane, k), NX - 1);
           R s1 = cg ? cs[a] : R(0);
           R s2 = sXg ? sXg[t * NX + a] : R(0);
           if constexpr (DIAG) {
@@ -402,14 +411,18 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
             s1 += ab * lm[b];
             s2 += ab * lh[b];
           }
-          nl = s1;
-          nh = s2;
+          nl[k] = s1;
+          nh[k] = s2;
         }
         __syncwarp(gm);
         adjp.release(t);
-        if (lane < NX) {
-          lams[lane] = nl;
-          lhs[lane] = nh;
+#pragma unroll
+        for (int k = 0; k < RPL; k++) {
+          const int a = row_of<G, RPL>(lane, k);
+          if (a < NX) {
+            lams[a] = nl[k];
+            lhs[a] = nh[k];
+          }
         }
         __syncwarp(gm);
       }
@@ -423,11 +436,15 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
     if (want_theta) {
       R* o = (R*)args.dtheta + (size_t)pid * args.n_theta;
       if constexpr (M::kLinearParams) {
-        if (lane < NX) {
 #pragma unroll
-          for (int j2 = 0; j2 < NX; j2++) o[lane * NX + j2] = grow[j2];
+        for (int k = 0; k < RPL; k++) {
+          const int a = row_of<G, RPL>(lane, k);
+          if (a < NX) {
 #pragma unroll
-          for (int j2 = 0; j2 < NU; j2++) o[NX * NX + lane * NU + j2] = grow[NX + j2];
+            for (int j2 = 0; j2 < NX; j2++) o[a * NX + j2] = grow[k][j2];
+#pragma unroll
+            for (int j2 = 0; j2 < NU; j2++) o[NX * NX + a * NU + j2] = grow[k][NX + j2];
+          }
         }
       } else if constexpr (M::NTH > 0) {
         if (lane == 0)

@@ -101,10 +101,11 @@ DMPC_DEV void step_e(const double* P, double dt, const R* As, int lda, const R* 
 }
 
 template <class M, int G, bool DIAG, class R>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2) ilqr_forward_kernel(const FwdArgs args) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD, XLD = D::XLD, ULD = D::ULD;
+  constexpr int RPL = (NX + G - 1) / G;  // state rows owned by each lane
   constexpr int NSLOT = G >= 4 ? 4 : G;  // concurrent line-search candidates
   constexpr int LC = G / NSLOT;          // lanes per candidate slot
   using Lay = FwdLayout<M, DIAG, R>;
@@ -277,9 +278,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
   int it = 0;
   for (; it < args.K_max && active; it++) {
     // ------------------- stage 1+2: fused linearise + Riccati sweep -------------
-    R vxx[NX];  // row `lane` of V_xx (value Hessian), carried across stages
+    R vxx[RPL][NX];  // the lane's rows of V_xx (value Hessian), carried across stages
 #pragma unroll
-    for (int b = 0; b < NX; b++) vxx[b] = R(0);
+    for (int k = 0; k < RPL; k++)
+#pragma unroll
+      for (int bb = 0; bb < NX; bb++) vxx[k][bb] = R(0);
     for (int e = lane; e < NX; e += G) S.Vx[e] = R(0);
     bwdp.start(T - 1);
     for (int t = T - 1; t >= 0; t--) {
@@ -302,12 +305,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
         if ((i % G) == lane) S.zs[i] = (i < NX) ? xr[i < NX ? i : 0] : ur[i >= NX ? i - NX : 0];
       __syncwarp(gm);
       // gz = C z + c ; qx = gz_x + A' Vx ; qu = gz_u + B' Vx   (kernels.py:395-410)
-      R qx = R(0);
+      R qx[RPL];
       R zv[NZ], vx[NX];
       lds_row<NZ>(S.zs, zv);
       lds_row<NX>(S.Vx, vx);
-      if (lane < NX) {
-        const int a = lane;
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int a = min(row_of<G, RPL>(lane, k), NX - 1);
         R s = cs[a];
         if constexpr (DIAG) {
           s += Cs[a] * S.zs[a];
@@ -315,14 +319,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
           R crow[NZ];
           lds_row<NZ>(Cs + a * ZLD, crow);
 #pragma unroll
-          for (int b = 0; b < NZ; b++) s += crow[b] * zv[b];
+          for (int b2 = 0; b2 < NZ; b2++) s += crow[b2] * zv[b2];
         }
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += S.As[b * LDA + a] * vx[b];
-        qx = s;
+        for (int b2 = 0; b2 < NX; b2++) s += S.As[b2 * LDA + a] * vx[b2];
+        qx[k] = s;
       }
-      if (lane < NU) {
-        const int a = lane;
+      for (int a = lane; a < NU; a += G) {
         R s = cs[NX + a];
         if constexpr (DIAG) {
           s += Cs[NX + a] * S.zs[NX + a];
@@ -330,17 +333,17 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
           R crow[NZ];
           lds_row<NZ>(Cs + (NX + a) * ZLD, crow);
 #pragma unroll
-          for (int b = 0; b < NZ; b++) s += crow[b] * zv[b];
+          for (int b2 = 0; b2 < NZ; b2++) s += crow[b2] * zv[b2];
         }
 #pragma unroll
-        for (int b = 0; b < NX; b++) s += S.Bs[b * LDB + a] * vx[b];
+        for (int b2 = 0; b2 < NX; b2++) s += S.Bs[b2 * LDB + a] * vx[b2];
         S.qu[a] = s;
       }
-      if (lane < NX) ric_MA_NB<M, DIAG, R>(S, lane, vxx);
+      ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx);
       __syncwarp(gm);
       for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU);
-      R quxc[NU], qxx[NX];
-      if (lane < NX) ric_Qxx_Qux<M, DIAG, R>(S, Cs, lane, qxx, quxc);
+      R quxc[RPL][NU], qxx[RPL][NX];
+      ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc);
       __syncwarp(gm);
       bwdp.release(t);  // C_t fully consumed: prefetch C_{t-1}
       // ---- stage QP on the control increment (type R, all lanes redundantly) ----
@@ -373,34 +376,36 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
           kg[t * ULD + i] = kd;
         }
       }
-      R kcol[NU];
-      if (lane < NX) {
-        const int b = lane;
+      R kcol[RPL][NU];
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int b2 = row_of<G, RPL>(lane, k);
         R rhs[NU], sol[NU];
 #pragma unroll
-        for (int i = 0; i < NU; i++) rhs[i] = fr[i] ? quxc[i] : R(0);
+        for (int i = 0; i < NU; i++) rhs[i] = fr[i] ? quxc[k][i] : R(0);
         chol_solve<NU, R>(ch, rhs, sol);
 #pragma unroll
-        for (int i = 0; i < NU; i++) {
-          kcol[i] = fr[i] ? -sol[i] : R(0);
-          Kg[(t * NU + i) * LDA + b] = kcol[i];
-        }
-        ric_publish_cols<M, DIAG, R>(S, b, kcol, quxc, quu);
-        // Vx update (kernels.py:491-498), unregularised Quu
-        R s = qx;
+        for (int i = 0; i < NU; i++) kcol[k][i] = fr[i] ? -sol[i] : R(0);
+        if (b2 < NX) {
 #pragma unroll
-        for (int r = 0; r < NU; r++) {
-          R rowq = R(0);
+          for (int i = 0; i < NU; i++) Kg[(t * NU + i) * LDA + b2] = kcol[k][i];
+          ric_publish_cols<M, DIAG, R>(S, b2, kcol[k], quxc[k], quu);
+          // Vx update (kernels.py:491-498), unregularised Quu
+          R s = qx[k];
 #pragma unroll
-          for (int q = 0; q < NU; q++) rowq += quu[r][q] * du[q];
-          s += kcol[r] * (rowq + qu_c[r]) + quxc[r] * du[r];
+          for (int r = 0; r < NU; r++) {
+            R rowq = R(0);
+#pragma unroll
+            for (int q = 0; q < NU; q++) rowq += quu[r][q] * du[q];
+            s += kcol[k][r] * (rowq + qu_c[r]) + quxc[k][r] * du[r];
+          }
+          S.Vx[b2] = s;  // all lanes finished reading Vx (qx/qu) before the last sync
         }
-        S.Vx[b] = s;  // all lanes finished reading Vx (qx/qu) before the last sync
       }
       __syncwarp(gm);
-      if (lane < NX) ric_Vxx_row<M, DIAG, R>(S, lane, qxx, kcol, quxc);
+      ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc);
       __syncwarp(gm);
-      if (lane < NX) ric_symmetrize<M, DIAG, R>(S, lane, vxx);
+      ric_symmetrize<M, DIAG, R, G, RPL>(S, lane, vxx);
     }
     cp_async_wait_all();
     __syncwarp(gm);
@@ -511,29 +516,37 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (M::NX <= 8 ? 4 : 3) : 2
       const double alpha = args.alphas[best];
       double xc[NX];
       lds_row_d<NX>(Xn, xc);
+      constexpr int NUR = (NU + G - 1) / G;
       for (int t = 0; t < T; t++) {
-        double v = 0.0;
-        if (lane < NU) {
-          const int r = lane;
-          double xbar[NX];
-          lds_row_d<NX>(Xn + t * XLD, xbar);
-          v = Un[t * ULD + r] + alpha * kg[t * ULD + r];
-          R krow[NX];
-          lds_row<NX>(Kg + (t * NU + r) * LDA, krow);
+        double v[NUR];
+        double xbar[NX];
+        lds_row_d<NX>(Xn + t * XLD, xbar);
 #pragma unroll
-          for (int b = 0; b < NX; b++) v += (double)krow[b] * (xc[b] - xbar[b]);
-          const double lo = args.u_min[r], hi = args.u_max[r];
-          if (v < lo) v = lo;
-          else if (v > hi) v = hi;
+        for (int m2 = 0; m2 < NUR; m2++) {
+          const int r = lane + m2 * G;
+          v[m2] = 0.0;
+          if (r < NU) {
+            double w = Un[t * ULD + r] + alpha * kg[t * ULD + r];
+            R krow[NX];
+            lds_row<NX>(Kg + (t * NU + r) * LDA, krow);
+#pragma unroll
+            for (int b = 0; b < NX; b++) w += (double)krow[b] * (xc[b] - xbar[b]);
+            const double lo = args.u_min[r], hi = args.u_max[r];
+            if (w < lo) w = lo;
+            else if (w > hi) w = hi;
+            v[m2] = w;
+          }
         }
         double u[NU];
 #pragma unroll
-        for (int r = 0; r < NU; r++) u[r] = __shfl_sync(gm, v, r, G);
+        for (int r = 0; r < NU; r++) u[r] = __shfl_sync(gm, v[r / G], r % G, G);
         __syncwarp(gm);
 #pragma unroll
         for (int i = 0; i < NX; i++)
           if ((i % G) == lane) Xn[t * XLD + i] = xc[i];
-        if (lane < NU) Un[t * ULD + lane] = v;
+#pragma unroll
+        for (int m2 = 0; m2 < NUR; m2++)
+          if (lane + m2 * G < NU) Un[t * ULD + lane + m2 * G] = v[m2];
         double xn[NX];
         step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
 #pragma unroll

@@ -16,7 +16,9 @@ int fail(const char* fmt, ...) __attribute__((format(printf, 1, 2)));
 extern std::atomic<int64_t> g_launches;
 int max_smem_optin();
 
-constexpr int group_size(int nx) { return nx <= 4 ? 4 : (nx <= 8 ? 8 : (nx <= 16 ? 16 : 32)); }
+// default lanes per problem (a lane owns ceil(n_x / G) state rows)
+constexpr int default_group(int nx) { return nx <= 4 ? 4 : (nx <= 8 ? 8 : 16); }
+int group_env();  // DIFFMPC_GROUP override (0 = none), read once
 
 
 template <class M>
@@ -25,22 +27,36 @@ int check_theta(const DiffMPCProblem* p) {
   return 0;
 }
 
-template <class Lay>
-int plan(int B, int T, int G, int& gpb, int& stride) {
+// Problems per block: among gpb in {128/G, 64/G, 32/G, ...} pick the one that keeps the
+// most problems resident per SM (occupancy API: registers + shared memory).
+template <class Lay, class K>
+int plan(K kern, int B, int T, int G, int& gpb, int& stride) {
   const Lay L = Lay::make(T);
   stride = L.total;
   const int limit = max_smem_optin();
-  gpb = 128 / G;
-  while (gpb > 1 && gpb * stride > limit) gpb--;
-  if (gpb * stride > limit)
+  int best = -1, best_res = -1;
+  for (int g = 128 / G; g >= 1; g /= 2) {
+    const int smem = g * stride;
+    if (smem > limit) continue;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, g * G, smem) != cudaSuccess) nb = 1;
+    const int res = nb * g;
+    if (res > best_res) {
+      best_res = res;
+      best = g;
+    }
+  }
+  cudaGetLastError();
+  if (best < 0)
     return fail("horizon T=%d needs %d bytes of shared memory per problem (limit %d)", T, stride, limit);
+  gpb = best;
   if (B < gpb) gpb = B > 0 ? B : 1;
   return 0;
 }
 
-template <class M, bool DIAG, class R>
+template <class M, int G, bool DIAG, class R>
 int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s) {
-  constexpr int G = group_size(M::NX);
   if (check_theta<M>(p)) return -1;
   if (!io || !io->X || !io->U || !io->J || !io->C || !io->c || !io->x0 || !io->U_warm ||
       (M::NTH > 0 && !io->theta))
@@ -58,9 +74,9 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   a.X = io->X; a.U = io->U; a.J = io->J; a.K = io->K; a.k = io->k; a.iters = io->iters;
   a.converged = io->converged; a.diverged = io->diverged; a.fail_t = io->fail_t;
   a.clamped = io->clamped; a.alpha_hist = io->alpha_hist; a.J_hist = io->J_hist;
-  if (plan<FwdLayout<M, DIAG, R>>(p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
-  const int smem = a.gpb * a.smem_stride;
   auto kern = ilqr_forward_kernel<M, G, DIAG, R>;
+  if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
+  const int smem = a.gpb * a.smem_stride;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int blocks = (p->B + a.gpb - 1) / a.gpb;
   kern<<<blocks, a.gpb * G, smem, s>>>(a);
@@ -70,9 +86,8 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   return 0;
 }
 
-template <class M, bool DIAG, class R>
+template <class M, int G, bool DIAG, class R>
 int bwd_impl(const DiffMPCProblem* p, const DiffMPCBackwardIO* io, cudaStream_t s) {
-  constexpr int G = group_size(M::NX);
   if (check_theta<M>(p)) return -1;
   if (!io || !io->C || !io->X || !io->U || !io->dc || (M::NTH > 0 && !io->theta))
     return fail("backward: required pointer is NULL");
@@ -88,9 +103,9 @@ int bwd_impl(const DiffMPCProblem* p, const DiffMPCBackwardIO* io, cudaStream_t 
   a.dLdX = io->dLdX; a.dLdU = io->dLdU; a.dLdJ = io->dLdJ;
   a.dC = io->dC; a.dc = io->dc; a.dx0 = io->dx0; a.dtheta = io->dtheta; a.dX = io->dX; a.dU = io->dU;
   a.fail_t = io->fail_t;
-  if (plan<BwdLayout<M, DIAG, R>>(p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
-  const int smem = a.gpb * a.smem_stride;
   auto kern = ilqr_backward_kernel<M, G, DIAG, R>;
+  if (plan<BwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
+  const int smem = a.gpb * a.smem_stride;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int blocks = (p->B + a.gpb - 1) / a.gpb;
   kern<<<blocks, a.gpb * G, smem, s>>>(a);
@@ -177,17 +192,39 @@ struct Call {
   cudaStream_t s;
 };
 
-template <class M, class R>
-int run(const Call& c) {
+template <class M, class R, int G>
+int run_g(const Call& c) {
   const bool diag = c.p->cost_layout == DIFFMPC_COST_DIAG;
   switch (c.op) {
     case Op::Fwd:
-      return diag ? fwd_impl<M, true, R>(c.p, c.fio, c.s) : fwd_impl<M, false, R>(c.p, c.fio, c.s);
+      return diag ? fwd_impl<M, G, true, R>(c.p, c.fio, c.s) : fwd_impl<M, G, false, R>(c.p, c.fio, c.s);
     case Op::Bwd:
-      return diag ? bwd_impl<M, true, R>(c.p, c.bio, c.s) : bwd_impl<M, false, R>(c.p, c.bio, c.s);
+      return diag ? bwd_impl<M, G, true, R>(c.p, c.bio, c.s) : bwd_impl<M, G, false, R>(c.p, c.bio, c.s);
     default:
       return dyn_impl<M, R>(c.p, c.N, c.theta, c.x, c.u, c.xn, c.A, c.Bm, c.s);
   }
+}
+
+// Lanes per problem: the default per model, or DIFFMPC_GROUP={4,8,16} (tuning / A-B).
+template <class M>
+int pick_group() {
+  const int env = group_env();
+  if (env == 4) return 4;
+  if (env == 8 && M::NX > 4) return 8;
+  if (env == 16 && M::NX > 8) return 16;
+  return default_group(M::NX);
+}
+
+template <class M, class R>
+int run(const Call& c) {
+  const int g = pick_group<M>();
+  if constexpr (M::NX > 8) {
+    if (g == 16) return run_g<M, R, 16>(c);
+  }
+  if constexpr (M::NX > 4) {
+    if (g == 8) return run_g<M, R, 8>(c);
+  }
+  return run_g<M, R, 4>(c);
 }
 
 }  // namespace dmpc

@@ -175,66 +175,91 @@ struct CostPipe {
 };
 
 // ---------------------------------------------------------------------------
-// MA = V_xx A, NB = V_xx B (row `a` from the lane's register row of V_xx)
-// (kernels.py:411-421 / 629-639)
+// Row-lane building blocks. A lane owns the RPL rows a_k = lane + k*G (k < RPL) of
+// every n_x x n_x quantity and the matching columns of the n_u x n_x ones; rows
+// a_k >= n_x are padding (computed on zeros, never stored). Every shared-memory row
+// fetched below is reused for all RPL rows of the lane.
 // ---------------------------------------------------------------------------
-template <class M, bool DIAG, class R>
-DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int a, const R (&vxx)[M::NX]) {
+template <int G, int RPL>
+DMPC_DEV int row_of(int lane, int k) { return lane + k * G; }
+
+// MA = V_xx A, NB = V_xx B  (kernels.py:411-421 / 629-639)
+template <class M, bool DIAG, class R, int G, int RPL>
+DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][M::NX]) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
-  R ma[NX], nb[NU];
+  R ma[RPL][NX], nb[RPL][NU];
 #pragma unroll
-  for (int b = 0; b < NX; b++) ma[b] = R(0);
+  for (int k = 0; k < RPL; k++) {
 #pragma unroll
-  for (int b = 0; b < NU; b++) nb[b] = R(0);
+    for (int b = 0; b < NX; b++) ma[k][b] = R(0);
+#pragma unroll
+    for (int b = 0; b < NU; b++) nb[k][b] = R(0);
+  }
 #pragma unroll
   for (int r = 0; r < NX; r++) {
     R arow[NX], brow[NU];
     lds_row<NX>(S.As + r * D::LDA, arow);
     lds_row<NU>(S.Bs + r * D::LDB, brow);
-    const R v = vxx[r];
 #pragma unroll
-    for (int b = 0; b < NX; b++) ma[b] += v * arow[b];
+    for (int k = 0; k < RPL; k++) {
+      const R v = vxx[k][r];
 #pragma unroll
-    for (int b = 0; b < NU; b++) nb[b] += v * brow[b];
+      for (int b = 0; b < NX; b++) ma[k][b] += v * arow[b];
+#pragma unroll
+      for (int b = 0; b < NU; b++) nb[k][b] += v * brow[b];
+    }
   }
 #pragma unroll
-  for (int b = 0; b < NX; b++) S.MA[a * D::LDA + b] = ma[b];
+  for (int k = 0; k < RPL; k++) {
+    const int a = row_of<G, RPL>(lane, k);
+    if (a < NX) {
 #pragma unroll
-  for (int b = 0; b < NU; b++) S.NB[a * D::LDB + b] = nb[b];
+      for (int b = 0; b < NX; b++) S.MA[a * D::LDA + b] = ma[k][b];
+#pragma unroll
+      for (int b = 0; b < NU; b++) S.NB[a * D::LDB + b] = nb[k][b];
+    }
+  }
 }
 
 // Q_xx row a = C_xx[a,:] + sum_r A[r,a] MA[r,:]  (kernels.py:422-427), and
 // Q_ux column a = C_ux[:,a] + sum_r B[r,:] MA[r,a] (kernels.py:428-433).
-template <class M, bool DIAG, class R>
-DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int a, R (&qxx)[M::NX], R (&quxc)[M::NU]) {
+template <class M, bool DIAG, class R, int G, int RPL>
+DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&qxx)[RPL][M::NX],
+                          R (&quxc)[RPL][M::NU]) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
-  if constexpr (DIAG) {
+  int ac[RPL];  // clamped row index (padding rows alias the last row; never stored)
 #pragma unroll
-    for (int bb = 0; bb < NX; bb++) qxx[bb] = R(0);
-    const R caa = Cs[a];
+  for (int k = 0; k < RPL; k++) {
+    const int a = row_of<G, RPL>(lane, k);
+    ac[k] = a < NX ? a : NX - 1;
+    if constexpr (DIAG) {
+      const R caa = Cs[ac[k]];
 #pragma unroll
-    for (int bb = 0; bb < NX; bb++)
-      if (bb == a) qxx[bb] = caa;
+      for (int bb = 0; bb < NX; bb++) qxx[k][bb] = (bb == ac[k]) ? caa : R(0);
 #pragma unroll
-    for (int i = 0; i < NU; i++) quxc[i] = R(0);
-  } else {
-    lds_row<NX>(Cs + a * D::ZLD, qxx);
+      for (int i = 0; i < NU; i++) quxc[k][i] = R(0);
+    } else {
+      lds_row<NX>(Cs + ac[k] * D::ZLD, qxx[k]);
 #pragma unroll
-    for (int i = 0; i < NU; i++) quxc[i] = Cs[(NX + i) * D::ZLD + a];
+      for (int i = 0; i < NU; i++) quxc[k][i] = Cs[(NX + i) * D::ZLD + ac[k]];
+    }
   }
 #pragma unroll
   for (int r = 0; r < NX; r++) {
     R mrow[NX], brow[NU];
     lds_row<NX>(S.MA + r * D::LDA, mrow);
     lds_row<NU>(S.Bs + r * D::LDB, brow);
-    const R ar = S.As[r * D::LDA + a];
-    const R mra = S.MA[r * D::LDA + a];
 #pragma unroll
-    for (int bb = 0; bb < NX; bb++) qxx[bb] += ar * mrow[bb];
+    for (int k = 0; k < RPL; k++) {
+      const R ar = S.As[r * D::LDA + ac[k]];
+      const R mra = S.MA[r * D::LDA + ac[k]];
 #pragma unroll
-    for (int i = 0; i < NU; i++) quxc[i] += brow[i] * mra;
+      for (int bb = 0; bb < NX; bb++) qxx[k][bb] += ar * mrow[bb];
+#pragma unroll
+      for (int i = 0; i < NU; i++) quxc[k][i] += brow[i] * mra;
+    }
   }
 }
 
@@ -254,8 +279,7 @@ DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j) {
   return s;
 }
 
-// After the gains: publish column a of K, Qux, Quu K; return nothing. The value
-// Hessian update then reads those columns for every b (kernels.py:499-507).
+// Publish column a of K, Qux and Quu K for the value-Hessian update.
 template <class M, bool DIAG, class R>
 DMPC_DEV void ric_publish_cols(const Ric<M, DIAG, R>& S, int a, const R (&kcol)[M::NU], const R (&quxc)[M::NU],
                                const R (&quu)[M::NU][M::NU]) {
@@ -272,10 +296,11 @@ DMPC_DEV void ric_publish_cols(const Ric<M, DIAG, R>& S, int a, const R (&kcol)[
   }
 }
 
-// newVxx row a -> N (aliases MA). s = Qxx[a,b] + sum_r (K_ra QuuK_rb + K_ra Qux_rb) + Qux_ra K_rb
-template <class M, bool DIAG, class R>
-DMPC_DEV void ric_Vxx_row(const Ric<M, DIAG, R>& S, int a, const R (&qxx)[M::NX], const R (&kcol)[M::NU],
-                          const R (&quxc)[M::NU]) {
+// newVxx rows -> N (aliases MA): s = Qxx[a,b] + sum_r (K_ra QuuK_rb + K_ra Qux_rb) + Qux_ra K_rb
+// (kernels.py:499-507)
+template <class M, bool DIAG, class R, int G, int RPL>
+DMPC_DEV void ric_Vxx_rows(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RPL][M::NX],
+                           const R (&kcol)[RPL][M::NU], const R (&quxc)[RPL][M::NU]) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
 #pragma unroll
@@ -284,22 +309,35 @@ DMPC_DEV void ric_Vxx_row(const Ric<M, DIAG, R>& S, int a, const R (&qxx)[M::NX]
     lds_row<NU>(S.QuuKT + bb * D::LDB, kq);
     lds_row<NU>(S.QuxT + bb * D::LDB, qx);
     lds_row<NU>(S.KT + bb * D::LDB, kk);
-    R s = qxx[bb];
 #pragma unroll
-    for (int r = 0; r < NU; r++) s += (kcol[r] * kq[r] + kcol[r] * qx[r]) + quxc[r] * kk[r];
-    S.MA[a * D::LDA + bb] = s;
+    for (int k = 0; k < RPL; k++) {
+      const int a = row_of<G, RPL>(lane, k);
+      R s = qxx[k][bb];
+#pragma unroll
+      for (int r = 0; r < NU; r++) s += (kcol[k][r] * kq[r] + kcol[k][r] * qx[r]) + quxc[k][r] * kk[r];
+      if (a < NX) S.MA[a * D::LDA + bb] = s;
+    }
   }
 }
 
-// V_xx row a = (N[a,:] + N[:,a]) / 2  (kernels.py:510-512)
-template <class M, bool DIAG, class R>
-DMPC_DEV void ric_symmetrize(const Ric<M, DIAG, R>& S, int a, R (&vxx)[M::NX]) {
+// V_xx rows = (N[a,:] + N[:,a]) / 2  (kernels.py:510-512); padding rows stay zero.
+template <class M, bool DIAG, class R, int G, int RPL>
+DMPC_DEV void ric_symmetrize(const Ric<M, DIAG, R>& S, int lane, R (&vxx)[RPL][M::NX]) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX;
-  R row[NX];
-  lds_row<NX>(S.MA + a * D::LDA, row);
 #pragma unroll
-  for (int bb = 0; bb < NX; bb++) vxx[bb] = R(0.5) * (row[bb] + S.MA[bb * D::LDA + a]);
+  for (int k = 0; k < RPL; k++) {
+    const int a = row_of<G, RPL>(lane, k);
+    if (a < NX) {
+      R row[NX];
+      lds_row<NX>(S.MA + a * D::LDA, row);
+#pragma unroll
+      for (int bb = 0; bb < NX; bb++) vxx[k][bb] = R(0.5) * (row[bb] + S.MA[bb * D::LDA + a]);
+    } else {
+#pragma unroll
+      for (int bb = 0; bb < NX; bb++) vxx[k][bb] = R(0);
+    }
+  }
 }
 
 }  // namespace dmpc
