@@ -244,6 +244,40 @@ template <int NU, class T>
 DMPC_DEV bool stage_qp(const T (&Quu)[NU][NU], const T (&qu)[NU], const T (&lo)[NU],
                        const T (&hi)[NU], int max_iter, T tol, T (&du)[NU],
                        bool (&fr)[NU], Chol<NU, T>& ch) {
+  // Interior fast path (lambda = 0). From u = 0 with lo < 0 < hi no coordinate is
+  // clamped, the Newton step -H^-1 g is taken at step 1 (Armijo holds with margin
+  // 0.4 g'H^-1 g), and when that point is strictly inside the box the reference's
+  // next iteration only refines it at round-off level (gnorm <= tol in double). So
+  // du = -H^-1 g, all coordinates free, and the factor of H is the one K needs.
+  {
+    bool inside = true, all_free[NU];
+    T gn = T(0);
+#pragma unroll
+    for (int a = 0; a < NU; a++) {
+      inside = inside && (lo[a] < T(0)) && (hi[a] > T(0));
+      all_free[a] = true;
+      gn += qu[a] * qu[a];
+    }
+    if (inside && chol_masked<NU, T>(Quu, T(0), all_free, ch)) {
+      T sol[NU];
+      chol_solve<NU, T>(ch, qu, sol);
+      bool strict = true;
+      T sdotg = T(0);
+#pragma unroll
+      for (int a = 0; a < NU; a++) {
+        strict = strict && (-sol[a] > lo[a]) && (-sol[a] < hi[a]);
+        sdotg -= sol[a] * qu[a];
+      }
+      if (strict && sdotg < T(0) && !(sqrt_(gn) <= tol)) {
+#pragma unroll
+        for (int a = 0; a < NU; a++) {
+          du[a] = -sol[a];
+          fr[a] = true;
+        }
+        return true;
+      }
+    }
+  }
   double lamd = 0.0;
   for (;;) {
     const T lam = (T)lamd;

@@ -36,6 +36,9 @@ struct DoubleIntegrator {
   static constexpr bool kLinearParams = false;
   template <class S>
   DMPC_DEV static void prep(const S*, S* P) { P[0] = S(0); }
+  // structural nonzeros of A = df/dx and B = df/du (compile-time; zero terms are skipped)
+  __host__ __device__ static constexpr bool a_nz(int r, int c) { return r == c || (r < D && c == r + D); }
+  __host__ __device__ static constexpr bool b_nz(int r, int c) { return r >= D && r - D == c; }
   template <class S>
   DMPC_DEV static void step(const S*, S dt, const S* x, const S* u, S* o) {
 #pragma unroll
@@ -69,6 +72,10 @@ struct DoubleIntegrator {
 struct PlanarQuad {
   static constexpr int NX = 6, NU = 2, NTH = 4, NP = 6, KIND = 1;
   static constexpr bool kLinearParams = false;
+  __host__ __device__ static constexpr bool a_nz(int r, int c) {
+    return r == c || (r < 3 && c == r + 3) || ((r == 3 || r == 4) && c == 2);
+  }
+  __host__ __device__ static constexpr bool b_nz(int r, int c) { return r >= 3 && c >= 0; }
   // P = [m, arm, I, g, 1/m, arm/I]
   template <class S>
   DMPC_DEV static void prep(const S* th, S* P) {
@@ -144,6 +151,13 @@ struct PlanarQuad {
 struct Quad13 {
   static constexpr int NX = 13, NU = 4, NTH = 7, NP = 15, KIND = 3;
   static constexpr bool kLinearParams = false;
+  __host__ __device__ static constexpr bool a_nz(int r, int c) {
+    return r == c || (r < 3 && c == r + 7) ||
+           (r >= 3 && r <= 6 && ((c >= 3 && c <= 6) || c >= 10)) ||   // quaternion kinematics
+           ((r == 7 || r == 8) && c >= 3 && c <= 6) || (r == 9 && (c == 4 || c == 5)) ||  // R(q) e3
+           (r >= 10 && c >= 10);                                       // gyroscopic terms
+  }
+  __host__ __device__ static constexpr bool b_nz(int r, int c) { return r >= 7 && c >= 0; }
   // P = [m, arm, Jx, Jy, Jz, kappa, g, 1/m, arm/sqrt2, 1/Jx, 1/Jy, 1/Jz, Jz-Jy, Jx-Jz, Jy-Jx]
   template <class S>
   DMPC_DEV static void prep(const S* th, S* P) {
@@ -291,6 +305,8 @@ struct Quad13 {
 template <int NX_, int NU_>
 struct LinearModel {
   static constexpr int NX = NX_, NU = NU_, NTH = NX_ * NX_ + NX_ * NU_, NP = 1, KIND = 2;
+  __host__ __device__ static constexpr bool a_nz(int, int) { return true; }  // dense
+  __host__ __device__ static constexpr bool b_nz(int, int) { return true; }
   static constexpr bool kLinearParams = true;
 };
 

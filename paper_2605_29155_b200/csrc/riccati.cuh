@@ -183,7 +183,16 @@ struct CostPipe {
 template <int G, int RPL>
 DMPC_DEV int row_of(int lane, int k) { return lane + k * G; }
 
-// MA = V_xx A, NB = V_xx B  (kernels.py:411-421 / 629-639)
+template <class M>
+__host__ __device__ constexpr bool b_row_nz(int r) {
+  bool any = false;
+  for (int c = 0; c < M::NU; c++) any = any || M::b_nz(r, c);
+  return any;
+}
+
+// MA = V_xx A, NB = V_xx B  (kernels.py:411-421 / 629-639). Terms on structural zeros of
+// A_t / B_t (M::a_nz / M::b_nz, compile-time) are skipped; the row of A is the same for
+// every lane, so the skipping is uniform (no divergence).
 template <class M, bool DIAG, class R, int G, int RPL>
 DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][M::NX]) {
   using D = Dims<M, DIAG, R>;
@@ -200,14 +209,16 @@ DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][
   for (int r = 0; r < NX; r++) {
     R arow[NX], brow[NU];
     lds_row<NX>(S.As + r * D::LDA, arow);
-    lds_row<NU>(S.Bs + r * D::LDB, brow);
+    if (b_row_nz<M>(r)) lds_row<NU>(S.Bs + r * D::LDB, brow);
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
       const R v = vxx[k][r];
 #pragma unroll
-      for (int b = 0; b < NX; b++) ma[k][b] += v * arow[b];
+      for (int b = 0; b < NX; b++)
+        if (M::a_nz(r, b)) ma[k][b] += v * arow[b];
 #pragma unroll
-      for (int b = 0; b < NU; b++) nb[k][b] += v * brow[b];
+      for (int b = 0; b < NU; b++)
+        if (M::b_nz(r, b)) nb[k][b] += v * brow[b];
     }
   }
 #pragma unroll
@@ -222,8 +233,10 @@ DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][
   }
 }
 
-// Q_xx row a = C_xx[a,:] + sum_r A[r,a] MA[r,:]  (kernels.py:422-427), and
-// Q_ux column a = C_ux[:,a] + sum_r B[r,:] MA[r,a] (kernels.py:428-433).
+// Q_xx row a = C_xx[a,:] + (A' V_xx A)[a,:]  (kernels.py:422-427) and Q_ux column a =
+// C_ux[:,a] + sum_r B[r,:] MA[r,a] (kernels.py:428-433). A' V_xx A is evaluated as
+// MA' A (V_xx is exactly symmetric), i.e. row a = sum_r MA[r,a] A[r,:]: the lane-uniform
+// operand is again a row of A, so its structural zeros are skipped without divergence.
 template <class M, bool DIAG, class R, int G, int RPL>
 DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&qxx)[RPL][M::NX],
                           R (&quxc)[RPL][M::NU]) {
@@ -248,17 +261,18 @@ DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&q
   }
 #pragma unroll
   for (int r = 0; r < NX; r++) {
-    R mrow[NX], brow[NU];
-    lds_row<NX>(S.MA + r * D::LDA, mrow);
-    lds_row<NU>(S.Bs + r * D::LDB, brow);
+    R arow[NX], brow[NU];
+    lds_row<NX>(S.As + r * D::LDA, arow);
+    if (b_row_nz<M>(r)) lds_row<NU>(S.Bs + r * D::LDB, brow);
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
-      const R ar = S.As[r * D::LDA + ac[k]];
       const R mra = S.MA[r * D::LDA + ac[k]];
 #pragma unroll
-      for (int bb = 0; bb < NX; bb++) qxx[k][bb] += ar * mrow[bb];
+      for (int bb = 0; bb < NX; bb++)
+        if (M::a_nz(r, bb)) qxx[k][bb] += mra * arow[bb];
 #pragma unroll
-      for (int i = 0; i < NU; i++) quxc[k][i] += brow[i] * mra;
+      for (int i = 0; i < NU; i++)
+        if (M::b_nz(r, i)) quxc[k][i] += brow[i] * mra;
     }
   }
 }
@@ -275,7 +289,8 @@ DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j) {
     s = Cs[(NX + i) * D::ZLD + NX + j];
   }
 #pragma unroll
-  for (int r = 0; r < NX; r++) s += S.Bs[r * D::LDB + i] * S.NB[r * D::LDB + j];
+  for (int r = 0; r < NX; r++)
+    if (b_row_nz<M>(r)) s += S.Bs[r * D::LDB + i] * S.NB[r * D::LDB + j];
   return s;
 }
 
