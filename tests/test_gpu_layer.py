@@ -140,12 +140,28 @@ def test_mpc_module_gradients_fd_linear():
         return (wx * x).sum() + (wu * u).sum() + 0.3 * J.sum()
 
     loss().backward()
+    # clamped controls at the solution (time-major like the module's outputs)
+    clamped = mpc.last_result.clamped.transpose(0, 1).cpu().numpy().astype(bool)
     eps = 1e-6
     worst = 0.0
+    n_checked_zero = 0
     # C is used as a symmetric matrix (gz = C z, kernels.py:395-399), so dC = sym(dz z') is the
     # gradient for symmetric perturbations: off-diagonal entries are perturbed in pairs.
-    for t, idx in [(C, (1, 0, 2, 2)), (C, (3, 1, 0, 4)), (c, (0, 1, 3)), (c, (4, 0, 1)), (x0, (1, 2)),
-                   (dx.params, (0,)), (dx.params, (10,))]:
+    for t, idx in [(C, (1, 0, 2, 2)), (C, (3, 1, 0, 4)), (C, (0, 0, 1, 3)), (C, (2, 1, 0, 1)),
+                   (c, (0, 1, 3)), (c, (4, 0, 1)), (x0, (1, 2)), (dx.params, (0,)), (dx.params, (10,))]:
+        if t is C and any(j >= n and clamped[idx[0], idx[1], j - n] for j in idx[2:]):
+            # Reference convention (kernels.py:733-756): rows/cols of dC on
+            # a clamped control are zeroed, dropping the 1/2 dz_x z_u cross term the exact
+            # derivative has. The x/u seeds contribute nothing there; only the optimal-cost
+            # (envelope) term 0.3 * 1/2 z z' remains.
+            x, u, _ = mpc(x0, QuadCost(C, c), dx)
+            z = torch.cat([x, u], -1)[idx[0], idx[1]]
+            mult = 1.0 if idx[2] == idx[3] else 2.0
+            env = 0.3 * 0.5 * mult * float(z[idx[2]] * z[idx[3]])
+            an = float(C.grad[idx]) + (float(C.grad[idx[0], idx[1], idx[3], idx[2]]) if mult == 2.0 else 0.0)
+            assert abs(an - env) <= 1e-9 * max(1.0, abs(env)), (idx, an, env)
+            n_checked_zero += 1
+            continue
         idxs = [idx]
         if t is C and idx[2] != idx[3]:
             idxs.append((idx[0], idx[1], idx[3], idx[2]))
@@ -162,6 +178,7 @@ def test_mpc_module_gradients_fd_linear():
         an = sum(float(t.grad[i]) for i in idxs)
         worst = max(worst, abs(fd - an) / max(1e-3, abs(fd)))
     assert worst <= 1e-4, worst
+    assert n_checked_zero >= 1  # the seed puts bound-active controls at (t=3, b=1)
 
 
 def test_mpc_module_theta_gradient_planar_envelope():
