@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define DIFFMPC_ABI_VERSION 1
+#define DIFFMPC_ABI_VERSION 2
 
 /* Model kinds. 0-2 follow dynamics.py:25-27 / kernels.py:24-26; 3 is the 13-state /
  * 4-rotor quadrotor that BASELINE.json names (no reference; defined in DESIGN.md). */
@@ -106,6 +106,10 @@ typedef struct DiffMPCForwardIO {
   uint8_t* clamped;        /* out (B,T,nu) (U<=u_min)|(U>=u_max) (ilqr.py:255)         */
   void* alpha_hist;        /* out (B,K_max) accepted alpha per iteration, 0 = no step  */
   void* J_hist;            /* out (B,K_max+1) cost after rollout and after each iteration (ilqr.py:202,244) */
+  void* workspace;         /* device scratch of >= diffmpc_forward_workspace_bytes() bytes, 256-byte
+                              aligned, or NULL: then the call allocates it stream-ordered
+                              (cudaMallocAsync / cudaFreeAsync on `stream`)                */
+  uint64_t workspace_bytes;
 } DiffMPCForwardIO;
 
 /* Implicit-differentiation backward I/O (one auxiliary LQR at the solution).
@@ -144,6 +148,11 @@ int diffmpc_dynamics_f32(const DiffMPCProblem* p, int32_t N, const void* theta, 
                          const void* u, void* xn, void* A, void* Bm, void* stream);
 int diffmpc_dynamics_f64(const DiffMPCProblem* p, int32_t N, const void* theta, const void* x,
                          const void* u, void* xn, void* A, void* Bm, void* stream);
+
+/* Bytes of device workspace one forward call needs (elem_bytes 4 for _f32, 8 for _f64):
+ * a work counter for the persistent grid plus the L2-resident feedback gains. This is the
+ * counterpart of the reference's preallocated Workspace gains arrays (ilqr.py:84-113). */
+uint64_t diffmpc_forward_workspace_bytes(const DiffMPCProblem* p, int32_t elem_bytes);
 
 /* 1 if (model_kind, nx, nu) has compiled kernels, else 0. */
 int diffmpc_supported(int32_t model_kind, int32_t nx, int32_t nu);

@@ -13,7 +13,7 @@ MAX_NU = 8
 MAX_ALPHA = 8
 COST_DENSE = 0
 COST_DIAG = 1
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class DiffMPCProblem(ctypes.Structure):
@@ -45,7 +45,8 @@ _vp = ctypes.c_void_p
 class DiffMPCForwardIO(ctypes.Structure):
     _fields_ = [(n, _vp) for n in (
         "theta", "C", "c", "x0", "U_warm", "X", "U", "J", "K", "k", "iters", "converged",
-        "diverged", "fail_t", "clamped", "alpha_hist", "J_hist")]
+        "diverged", "fail_t", "clamped", "alpha_hist", "J_hist", "workspace")] + [
+        ("workspace_bytes", ctypes.c_uint64)]
 
 
 class DiffMPCBackwardIO(ctypes.Structure):

@@ -15,6 +15,9 @@ from . import _abi
 from .errors import ConfigError, ExtensionMissingError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdiffmpc.so")
+# development A/B aid: load another in-tree build of the same ABI (tools/ab_*.sh)
+if os.environ.get("DIFFMPC_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["DIFFMPC_LIB"])
 _lock = threading.Lock()
 _lib = None
 
@@ -48,6 +51,8 @@ def lib():
             f = getattr(L, f"diffmpc_dynamics_{dt}")
             f.argtypes = [vp, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp]
             f.restype = ctypes.c_int
+        L.diffmpc_forward_workspace_bytes.argtypes = [vp, ctypes.c_int32]
+        L.diffmpc_forward_workspace_bytes.restype = ctypes.c_uint64
         L.diffmpc_supported.argtypes = [ctypes.c_int32] * 3
         L.diffmpc_supported.restype = ctypes.c_int
         L.diffmpc_launch_count.argtypes = []

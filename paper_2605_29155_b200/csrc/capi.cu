@@ -50,6 +50,16 @@ int group_env() {
   return v;
 }
 
+int num_sms() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 1;
+  }
+  return v;
+}
+
 int max_smem_optin() {
   static int v = -1;
   if (v < 0) {
@@ -149,6 +159,10 @@ int diffmpc_dynamics_f64(const DiffMPCProblem* p, int32_t N, const void* theta, 
                          void* xn, void* A, void* Bm, void* stream) {
   Call c{Op::Dyn, p, nullptr, nullptr, N, theta, x, u, xn, A, Bm, (cudaStream_t)stream};
   return entry<double>(c);
+}
+uint64_t diffmpc_forward_workspace_bytes(const DiffMPCProblem* p, int32_t elem_bytes) {
+  if (!p || (elem_bytes != 4 && elem_bytes != 8) || p->B < 0 || p->T < 1) return 0;
+  return (uint64_t)fwd_workspace_bytes(p->B, p->T, p->nx, p->nu, elem_bytes, p->cost_layout == DIFFMPC_COST_DIAG);
 }
 int diffmpc_supported(int32_t model_kind, int32_t nx, int32_t nu) { return supported(model_kind, nx, nu) ? 1 : 0; }
 int64_t diffmpc_launch_count(void) { return g_launches.load(); }

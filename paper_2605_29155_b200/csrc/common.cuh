@@ -38,6 +38,12 @@ DMPC_DEV void cp_async_elem(double* dst, const double* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
 }
+// 16-byte global -> shared copy that bypasses L1 (.cg): used for data this kernel itself
+// wrote to global memory earlier (the gain workspace), so no stale L1 line can be hit.
+DMPC_DEV void cp_async_16cg(void* dst, const void* src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
 DMPC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 DMPC_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -243,7 +249,8 @@ DMPC_DEV int boxqp(const T (&H)[NU][NU], T lam, const T (&g)[NU], const T (&lo)[
 template <int NU, class T>
 DMPC_DEV bool stage_qp(const T (&Quu)[NU][NU], const T (&qu)[NU], const T (&lo)[NU],
                        const T (&hi)[NU], int max_iter, T tol, T (&du)[NU],
-                       bool (&fr)[NU], Chol<NU, T>& ch) {
+                       bool (&fr)[NU], Chol<NU, T>& ch, bool& lam0) {
+  lam0 = true;
   // Interior fast path (lambda = 0). From u = 0 with lo < 0 < hi no coordinate is
   // clamped, the Newton step -H^-1 g is taken at step 1 (Armijo holds with margin
   // 0.4 g'H^-1 g), and when that point is strictly inside the box the reference's
@@ -304,6 +311,7 @@ DMPC_DEV bool stage_qp(const T (&Quu)[NU][NU], const T (&qu)[NU], const T (&lo)[
       if (chol_masked<NU, T>(Quu, lam, fr, ch)) return true;
     }
     lamd = (lamd == 0.0) ? kLamInit : lamd * 10.0;
+    lam0 = false;
     if (lamd > kLamMax) return false;
   }
 }

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         if (b2 < NX) {
 #pragma unroll
           for (int i = 0; i < NU; i++) Ka[(t * NU + i) * LDA + b2] = kcol[k][i];
-          ric_publish_cols<M, DIAG, R>(S, b2, kcol[k], quxc[k], quu);
+          ric_publish_cols<M, DIAG, R>(S, b2, kcol[k], quxc[k], true);
           R s = qx[k];
 #pragma unroll
           for (int r = 0; r < NU; r++) {
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         }
       }
       __syncwarp(gm);
-      ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc);
+      ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc, quu, true);
       __syncwarp(gm);
       ric_symmetrize<M, DIAG, R, G, RPL>(S, lane, vxx);
     }

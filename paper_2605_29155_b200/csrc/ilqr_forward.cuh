@@ -22,8 +22,17 @@
 // QP run in double — the iteration-count-critical quantities (SURVEY.md §7 hard
 // part 2, probes P7/P8).
 //
-// Shared-memory layout per problem (FwdLayout): nominal X/U and k (double), K (R),
-// Riccati scratch (R), two C_t staging buffers (R).
+// Shared-memory layout per problem (FwdLayout): nominal X/U and k (double), a shadow
+// X/U (double) that the first line-search candidate writes its trajectory into (so
+// accepting it is a pointer swap, no re-roll), the K_t staging buffer(s), the Riccati
+// scratch (R) and the C_t staging buffer(s) (R). The gains K live in an L2-resident
+// global workspace ([problem][t][n_u][LDA], written by the sweep, streamed back per
+// stage by the line search), which keeps ~8.5 KB of shared memory per 13-state problem.
+//
+// Scheduling: a persistent grid (resident blocks only). Each warp claims the next
+// 32/G problems with one atomicAdd on a per-launch counter and solves them in lockstep;
+// a warp whose problems converge early claims more work instead of idling until the
+// slowest problem of its block is done.
 #pragma once
 #include <type_traits>
 
@@ -52,6 +61,10 @@ struct FwdArgs {
   uint8_t* clamped;
   void* alpha_hist;
   void* J_hist;
+  void* Kw;            // gain workspace (B, T, NU, LDA) of R
+  void* Pw;            // packed cost records (B, T, REC) of R
+  int* ctr;            // per-launch work counter (zeroed before the launch)
+  int pw;              // problems per warp claimed by one atomicAdd (32/G, or gpb if smaller)
 };
 
 __host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a * a; }
@@ -59,7 +72,7 @@ __host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a *
 template <class M, bool DIAG, class R>
 struct FwdLayout {
   using D = Dims<M, DIAG, R>;
-  int oPe, oPr, oXn, oUn, okg, oKg, total;
+  int oPe, oPr, oXn, oUn, oUs, okg, oKb, total;
   RicLayout<M, DIAG, R> ric;
   __host__ __device__ static FwdLayout make(int T) {
     FwdLayout L;
@@ -68,9 +81,10 @@ struct FwdLayout {
     L.oPr = o; o += align_up(M::NP * (int)sizeof(R), 16);
     L.oXn = o; o += (T + 1) * D::XLD * 8;
     L.oUn = o; o += T * D::ULD * 8;
+    L.oUs = o; o += T * D::ULD * 8;
     L.okg = o; o += T * D::ULD * 8;
     o = align_up(o, 16);
-    L.oKg = o; o += T * D::NU * D::LDA * (int)sizeof(R);
+    L.oKb = o; o += D::NBUF * D::NU * D::LDA * (int)sizeof(R);
     o = align_up(o, 16);
     L.ric = RicLayout<M, DIAG, R>::make(o);
     L.total = align_up(L.ric.end, 16);
@@ -100,8 +114,22 @@ DMPC_DEV void step_e(const double* P, double dt, const R* As, int lda, const R* 
   }
 }
 
+// Feedback law v + K_r (x - xbar) in double (kernels.py:560-568) as two independent DFMA
+// chains; the line search and the winner's re-roll share it, so the re-roll reproduces
+// the candidate bit for bit.
+template <int NX, class R>
+DMPC_DEV double feedback(double v, const R (&krow)[NX], const double (&x)[NX], const double (&xbar)[NX]) {
+  double v1 = 0.0;
+#pragma unroll
+  for (int b = 0; b < NX; b++) {
+    if (b & 1) v1 += (double)krow[b] * (x[b] - xbar[b]);
+    else v += (double)krow[b] * (x[b] - xbar[b]);
+  }
+  return v + v1;
+}
+
 template <class M, int G, bool DIAG, class R>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (DIAG || M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD, XLD = D::XLD, ULD = D::ULD;
@@ -113,23 +141,47 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
   const int lane = threadIdx.x % G;
-  const int pid = blockIdx.x * args.gpb + grp;
-  if (grp >= args.gpb || pid >= args.B) return;
+  if (grp >= args.gpb) return;
   const unsigned gm = group_mask<G>();
+  // warp-level work claiming: the warp's `pw` groups take consecutive problems
+  const int pw = args.pw;
+  const int wlanes = pw * G;  // live lanes of this warp
+  const unsigned wmask = wlanes >= 32 ? 0xffffffffu : ((1u << wlanes) - 1u);
+  const int gi = (threadIdx.x & 31) / G;  // group index within the warp
   const int T = args.T;
   const Lay L = Lay::make(T);
   unsigned char* base = smem_raw + (size_t)grp * args.smem_stride;
-  double* Xn = (double*)(base + L.oXn);
-  double* Un = (double*)(base + L.oUn);
+  double* const Xn = (double*)(base + L.oXn);
+  double* const Ubuf0 = (double*)(base + L.oUn);
+  double* const Ubuf1 = (double*)(base + L.oUs);
   double* kg = (double*)(base + L.okg);
-  R* Kg = (R*)(base + L.oKg);
+  R* Kb = (R*)(base + L.oKb);
   Ric<M, DIAG, R> S;
   S.bind(base, L.ric);
+  const int units = (args.B + pw - 1) / pw;
 
+  auto claim = [&]() -> int {
+    int u = 0;
+    if ((threadIdx.x & 31) == 0) u = atomicAdd(args.ctr, 1);
+    return __shfl_sync(wmask, u, 0);
+  };
+
+  for (int unit = claim(); unit < units; unit = claim()) {
+  const int pid = unit * pw + gi;
+  if (pid < args.B) {
+  double* Un = Ubuf0;  // nominal controls (swapped with the alpha_0 candidate's on accept)
+  double* Us = Ubuf1;
   const R* Cg = (const R*)args.C + (size_t)pid * T * D::NCS;
   const R* cg = (const R*)args.c + (size_t)pid * T * NZ;
+  R* Kw = (R*)args.Kw + (size_t)pid * T * NU * LDA;
+  R* Ko = args.K ? (R*)args.K + (size_t)pid * T * NU * NX : nullptr;
+  // the initial rollout stages C_t / c_t element-wise from the caller's arrays and writes
+  // them out as packed, 16-byte aligned records (Pw); every later sweep and line search
+  // stages those with 16-byte copies
+  R* Pw = (R*)args.Pw + (size_t)pid * T * CostPipe<M, DIAG, R, G>::REC;
   CostPipe<M, DIAG, R, G> fwdp{&S, Cg, cg, T, lane, +1};
-  CostPipe<M, DIAG, R, G> bwdp{&S, Cg, cg, T, lane, -1};
+  CostPipe<M, DIAG, R, G> bwdp{&S, Cg, cg, T, lane, -1, nullptr, nullptr, Pw};
+  CostPipe<M, DIAG, R, G> lsp{&S, Cg, cg, T, lane, +1, Kw, Kb, Pw};
 
   // ---- parameters (prepared: raw + reciprocals), kept in shared memory ----
   const R* thg = (const R*)args.theta + (size_t)args.theta_stride * pid;
@@ -181,8 +233,6 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       Un[t * ULD + r] = v;
       kg[t * ULD + r] = 0.0;
     }
-    #pragma unroll 1
-    for (int e = lane; e < T * NU * LDA; e += G) Kg[e] = R(0);
   }
   __syncwarp(gm);
 
@@ -213,9 +263,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         if (i < NZ) {
           R crow[NZ];
           lds_row<NZ>(Cs + i * ZLD, crow);
-          double row = 0.0;
+          double ra[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent DFMA chains
 #pragma unroll
-          for (int jj = 0; jj < NZ; jj++) row += (double)crow[jj] * z[jj];
+          for (int jj = 0; jj < NZ; jj++) ra[jj & 3] += (double)crow[jj] * z[jj];
+          const double row = (ra[0] + ra[1]) + (ra[2] + ra[3]);
           double zi = 0.0;
 #pragma unroll
           for (int k = 0; k < LCX; k++)
@@ -231,6 +282,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
 
   double J = 0.0;
   int active = 1, fail_t = -1, iterations = 0, converged = 0, diverged = 0;
+  int k_lo = T;  // gains output rows [k_lo, T) were written by some sweep
   R* ahist = args.alpha_hist ? (R*)args.alpha_hist + (size_t)pid * args.K_max : nullptr;
   R* jhist = args.J_hist ? (R*)args.J_hist + (size_t)pid * (args.K_max + 1) : nullptr;
   if (ahist)
@@ -244,6 +296,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     for (int t = 0; t < T; t++) {
       fwdp.acquire(t);
       __syncwarp(gm);
+      fwdp.pack_out(Pw, t);
       double u[NU];
       lds_row_d<NU>(Un + t * ULD, u);
       J += stage_cost(std::integral_constant<int, G>{}, fwdp.C(t), fwdp.c(t), xc, u, lane, gm);
@@ -312,32 +365,33 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
 #pragma unroll
       for (int k = 0; k < RPL; k++) {
         const int a = min(row_of<G, RPL>(lane, k), NX - 1);
-        R s = cs[a];
+        R sa[4] = {cs[a], R(0), R(0), R(0)};  // independent FMA chains
         if constexpr (DIAG) {
-          s += Cs[a] * S.zs[a];
+          sa[1] = Cs[a] * S.zs[a];
         } else {
           R crow[NZ];
           lds_row<NZ>(Cs + a * ZLD, crow);
 #pragma unroll
-          for (int b2 = 0; b2 < NZ; b2++) s += crow[b2] * zv[b2];
+          for (int b2 = 0; b2 < NZ; b2++) sa[b2 & 1] += crow[b2] * zv[b2];
         }
 #pragma unroll
-        for (int b2 = 0; b2 < NX; b2++) s += S.As[b2 * LDA + a] * vx[b2];
-        qx[k] = s;
+        for (int b2 = 0; b2 < NX; b2++) sa[2 + (b2 & 1)] += S.As[b2 * LDA + a] * vx[b2];
+        qx[k] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
       }
       for (int a = lane; a < NU; a += G) {
-        R s = cs[NX + a];
+        R sa[4] = {cs[NX + a], R(0), R(0), R(0)};
         if constexpr (DIAG) {
-          s += Cs[NX + a] * S.zs[NX + a];
+          sa[1] = Cs[NX + a] * S.zs[NX + a];
         } else {
           R crow[NZ];
           lds_row<NZ>(Cs + (NX + a) * ZLD, crow);
 #pragma unroll
-          for (int b2 = 0; b2 < NZ; b2++) s += crow[b2] * zv[b2];
+          for (int b2 = 0; b2 < NZ; b2++) sa[b2 & 1] += crow[b2] * zv[b2];
         }
 #pragma unroll
-        for (int b2 = 0; b2 < NX; b2++) s += S.Bs[b2 * LDB + a] * vx[b2];
-        S.qu[a] = s;
+        for (int b2 = 0; b2 < NX; b2++)
+          if (b_row_nz<M>(b2)) sa[2 + (b2 & 1)] += S.Bs[b2 * LDB + a] * vx[b2];
+        S.qu[a] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
       }
       ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx);
       __syncwarp(gm);
@@ -348,7 +402,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       bwdp.release(t);  // C_t fully consumed: prefetch C_{t-1}
       // ---- stage QP on the control increment (type R, all lanes redundantly) ----
       R quu[NU][NU], qu_c[NU], lo[NU], hi[NU], du[NU];
-      bool fr[NU];
+      bool fr[NU], lam0;
       Chol<NU, R> ch;
 #pragma unroll
       for (int i = 0; i < NU; i++) {
@@ -357,7 +411,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         lo[i] = (R)(args.u_min[i] - ud[i]);
         hi[i] = (R)(args.u_max[i] - ud[i]);
       }
-      const bool ok = stage_qp<NU, R>(quu, qu_c, lo, hi, args.boxqp_max_iter, (R)args.boxqp_tol, du, fr, ch);
+      const bool ok = stage_qp<NU, R>(quu, qu_c, lo, hi, args.boxqp_max_iter, (R)args.boxqp_tol, du, fr, ch, lam0);
       if (!ok) {
         fail_t = t;
         active = 0;
@@ -388,8 +442,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         for (int i = 0; i < NU; i++) kcol[k][i] = fr[i] ? -sol[i] : R(0);
         if (b2 < NX) {
 #pragma unroll
-          for (int i = 0; i < NU; i++) Kg[(t * NU + i) * LDA + b2] = kcol[k][i];
-          ric_publish_cols<M, DIAG, R>(S, b2, kcol[k], quxc[k], quu);
+          for (int i = 0; i < NU; i++) Kw[(t * NU + i) * LDA + b2] = kcol[k][i];
+          if (Ko) {  // the gains output holds the last computed K (ilqr.py:264)
+#pragma unroll
+            for (int i = 0; i < NU; i++) Ko[(t * NU + i) * NX + b2] = kcol[k][i];
+          }
+          ric_publish_cols<M, DIAG, R>(S, b2, kcol[k], quxc[k], lam0);
           // Vx update (kernels.py:491-498), unregularised Quu
           R s = qx[k];
 #pragma unroll
@@ -402,8 +460,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           S.Vx[b2] = s;  // all lanes finished reading Vx (qx/qu) before the last sync
         }
       }
+      k_lo = t;
       __syncwarp(gm);
-      ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc);
+      ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc, quu, lam0);
       __syncwarp(gm);
       ric_symmetrize<M, DIAG, R, G, RPL>(S, lane, vxx);
     }
@@ -421,6 +480,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       Jc[a] = 0.0;
       dead[a] = false;
     }
+    const bool inplace = args.n_alpha <= NSLOT;  // one round: alpha_0 may overwrite X
     if (active) {
       const int NA = args.n_alpha;
       for (int round = 0; round * NSLOT < NA; round++) {
@@ -430,9 +490,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         lds_row_d<NX>(Xn, xc);
         double Jm = 0.0;
         bool dm = false;
-        fwdp.start(0);
+        // alpha_0 keeps its trajectory: controls in Us, states written over the nominal
+        // X_t once every slot has read it (restored by a re-roll if alpha_0 loses)
+        const bool shadow = inplace && (slot == 0);
+        lsp.start(0);
         for (int t = 0; t < T; t++) {
-          fwdp.acquire(t);
+          lsp.acquire(t);
           __syncwarp(gm);
           // feedback law u = clip(U + alpha k + K (x - X)) (kernels.py:560-568)
           constexpr int NUL = (NU + LC - 1) / LC;
@@ -446,12 +509,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
             if (r < NU) {
               v = Un[t * ULD + r] + alpha * kg[t * ULD + r];
               R krow[NX];
-              lds_row<NX>(Kg + (t * NU + r) * LDA, krow);
-#pragma unroll
-              for (int b = 0; b < NX; b++) v += (double)krow[b] * (xc[b] - xbar[b]);
+              lds_row<NX>(lsp.K(t) + r * LDA, krow);
+              v = feedback<NX>(v, krow, xc, xbar);
               const double lo = args.u_min[r], hi = args.u_max[r];
               if (v < lo) v = lo;
               else if (v > hi) v = hi;
+              if (shadow) Us[t * ULD + r] = v;
             }
             urr[rr] = v;
           }
@@ -459,9 +522,14 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
 #pragma unroll
           for (int r = 0; r < NU; r++)
             u[r] = (LC == 1) ? urr[r] : __shfl_sync(smask, urr[r / LC], (lane & ~(LC - 1)) + (r % LC), G);
-          Jm += stage_cost(std::integral_constant<int, LC>{}, fwdp.C(t), fwdp.c(t), xc, u, j, smask);
-          __syncwarp(gm);
-          fwdp.release(t);
+          Jm += stage_cost(std::integral_constant<int, LC>{}, lsp.C(t), lsp.c(t), xc, u, j, smask);
+          __syncwarp(gm);  // every slot has read the nominal X_t
+          if (shadow) {
+#pragma unroll
+            for (int i = 0; i < NX; i++)
+              if ((i % LC) == j) Xn[t * XLD + i] = xc[i];
+          }
+          lsp.release(t);
           double xn[NX];
           step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
           bool fin = finite_(Jm);
@@ -472,6 +540,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           }
           dm |= !fin;  // dead candidates keep stepping (harmlessly) to stay in lockstep
           __syncwarp(gm);
+        }
+        if (shadow) {
+#pragma unroll
+          for (int i = 0; i < NX; i++)
+            if ((i % LC) == j) Xn[T * XLD + i] = xc[i];
         }
         cp_async_wait_all();
         if (dm) Jm = INFINITY;
@@ -509,52 +582,83 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     const bool all_dead = act && alld;
     const bool accept = act && !all_dead && (best_J < J);
     if (ahist && lane == 0) ahist[it] = accept ? (R)args.alphas[best] : R(0);
-    if (accept) {
-      // re-roll the winning candidate (bit-identical to its line-search pass) and
-      // adopt it as the nominal trajectory; writes to X_t are delayed until the
-      // feedback at t has read the old nominal X_t.
+    const bool inplace_used = act && inplace;  // the nominal X now holds alpha_0's states
+    if (accept && best == 0 && inplace_used) {
+      // adopt the alpha_0 candidate: its states are already in X, its controls in Us
+      __syncwarp(gm);
+      double* tu = Un; Un = Us; Us = tu;
+    } else if (accept || inplace_used) {
+      // Re-roll the nominal (xb, bit-identical to the rollout that produced it: restores X
+      // after alpha_0 overwrote it) and, on accept, the winning candidate (xw, bit-identical
+      // to its line-search pass), adopting the latter. Writes to X_t / U_t are delayed until
+      // every lane has read the old U_t.
       const double alpha = args.alphas[best];
-      double xc[NX];
-      lds_row_d<NX>(Xn, xc);
+      double xw[NX], xb[NX];
+      lds_row_d<NX>(Xn, xb);
+#pragma unroll
+      for (int i = 0; i < NX; i++) xw[i] = xb[i];
       constexpr int NUR = (NU + G - 1) / G;
+      #pragma unroll 1
       for (int t = 0; t < T; t++) {
-        double v[NUR];
-        double xbar[NX];
-        lds_row_d<NX>(Xn + t * XLD, xbar);
+        double ub[NU];
+        lds_row_d<NU>(Un + t * ULD, ub);
+        double v[NUR], uw[NU];
 #pragma unroll
-        for (int m2 = 0; m2 < NUR; m2++) {
-          const int r = lane + m2 * G;
-          v[m2] = 0.0;
-          if (r < NU) {
-            double w = Un[t * ULD + r] + alpha * kg[t * ULD + r];
-            R krow[NX];
-            lds_row<NX>(Kg + (t * NU + r) * LDA, krow);
+        for (int r = 0; r < NU; r++) uw[r] = ub[r];
+        if (accept) {
 #pragma unroll
-            for (int b = 0; b < NX; b++) w += (double)krow[b] * (xc[b] - xbar[b]);
-            const double lo = args.u_min[r], hi = args.u_max[r];
-            if (w < lo) w = lo;
-            else if (w > hi) w = hi;
-            v[m2] = w;
+          for (int m2 = 0; m2 < NUR; m2++) {
+            const int r = lane + m2 * G;
+            v[m2] = 0.0;
+            if (r < NU) {
+              double w = Un[t * ULD + r] + alpha * kg[t * ULD + r];
+              R krow[NX];
+              if constexpr (sizeof(R) == 4) {
+                const float4* kr4 = reinterpret_cast<const float4*>(Kw + (t * NU + r) * LDA);
+#pragma unroll
+                for (int q = 0; q < (NX + 3) / 4; q++) {
+                  const float4 v4 = __ldcg(kr4 + q);
+                  const float tt[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                  for (int i = 0; i < 4; i++)
+                    if (q * 4 + i < NX) krow[q * 4 + i] = tt[i];
+                }
+              } else {
+#pragma unroll
+                for (int b = 0; b < NX; b++) krow[b] = __ldcg((const double*)(Kw + (t * NU + r) * LDA + b));
+              }
+              w = feedback<NX>(w, krow, xw, xb);
+              const double lo = args.u_min[r], hi = args.u_max[r];
+              if (w < lo) w = lo;
+              else if (w > hi) w = hi;
+              v[m2] = w;
+            }
           }
-        }
-        double u[NU];
 #pragma unroll
-        for (int r = 0; r < NU; r++) u[r] = __shfl_sync(gm, v[r / G], r % G, G);
+          for (int r = 0; r < NU; r++) uw[r] = __shfl_sync(gm, v[r / G], r % G, G);
+        }
         __syncwarp(gm);
 #pragma unroll
         for (int i = 0; i < NX; i++)
-          if ((i % G) == lane) Xn[t * XLD + i] = xc[i];
+          if ((i % G) == lane) Xn[t * XLD + i] = accept ? xw[i] : xb[i];
+        if (accept) {
 #pragma unroll
-        for (int m2 = 0; m2 < NUR; m2++)
-          if (lane + m2 * G < NU) Un[t * ULD + lane + m2 * G] = v[m2];
+          for (int m2 = 0; m2 < NUR; m2++)
+            if (lane + m2 * G < NU) Un[t * ULD + lane + m2 * G] = v[m2];
+        }
         double xn[NX];
-        step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
+        step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xb, ub, xn);
 #pragma unroll
-        for (int i = 0; i < NX; i++) xc[i] = xn[i];
+        for (int i = 0; i < NX; i++) xb[i] = xn[i];
+        if (accept) {
+          step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xw, uw, xn);
+#pragma unroll
+          for (int i = 0; i < NX; i++) xw[i] = xn[i];
+        }
       }
 #pragma unroll
       for (int i = 0; i < NX; i++)
-        if ((i % G) == lane) Xn[T * XLD + i] = xc[i];
+        if ((i % G) == lane) Xn[T * XLD + i] = accept ? xw[i] : xb[i];
       __syncwarp(gm);
     }
     const double J_prev = J;
@@ -593,10 +697,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         co[e] = (uint8_t)(v <= args.u_min[r] || v >= args.u_max[r]);
       }
     }
-    if (args.K) {
-      R* Ko = (R*)args.K + (size_t)pid * T * NU * NX;
+    if (Ko && k_lo > 0) {  // stages no sweep reached keep the zero-initialised gains
       #pragma unroll 1
-      for (int e = lane; e < T * NU * NX; e += G) Ko[e] = Kg[(e / NX) * LDA + e % NX];
+      for (int e = lane; e < k_lo * NU * NX; e += G) Ko[e] = R(0);
     }
     if (args.k) {
       R* ko = (R*)args.k + (size_t)pid * T * NU;
@@ -611,6 +714,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       if (args.fail_t) args.fail_t[pid] = fail_t;
     }
   }
+  __syncwarp(gm);
+  }  // pid < B
+  }  // persistent loop
 }
 
 }  // namespace dmpc

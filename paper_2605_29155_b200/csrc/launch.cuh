@@ -30,7 +30,7 @@ int check_theta(const DiffMPCProblem* p) {
 // Problems per block: among gpb in {128/G, 64/G, 32/G, ...} pick the one that keeps the
 // most problems resident per SM (occupancy API: registers + shared memory).
 template <class Lay, class K>
-int plan(K kern, int B, int T, int G, int& gpb, int& stride) {
+int plan(K kern, int B, int T, int G, int& gpb, int& stride, int* per_sm = nullptr) {
   const Lay L = Lay::make(T);
   stride = L.total;
   const int limit = max_smem_optin();
@@ -45,6 +45,7 @@ int plan(K kern, int B, int T, int G, int& gpb, int& stride) {
     if (res > best_res) {
       best_res = res;
       best = g;
+      if (per_sm) *per_sm = nb;
     }
   }
   cudaGetLastError();
@@ -53,6 +54,24 @@ int plan(K kern, int B, int T, int G, int& gpb, int& stride) {
   gpb = best;
   if (B < gpb) gpb = B > 0 ? B : 1;
   return 0;
+}
+
+int num_sms();
+
+// Forward workspace: [work counter (256 B)] [gains K (B, T, NU, LDA) of R]
+//                    [packed cost records (B, T, REC) of R]
+inline size_t fwd_gain_bytes(int B, int T, int nx, int nu, int elem) {
+  const int vn = 16 / elem;
+  const size_t lda = (size_t)((nx + vn - 1) / vn * vn);
+  return (size_t)B * T * nu * lda * elem;
+}
+inline size_t fwd_rec_elems(int nx, int nu, int elem, bool diag) {
+  const int vn = 16 / elem, nz = nx + nu;
+  const size_t zld = (size_t)((nz + vn - 1) / vn * vn);
+  return (diag ? zld : nz * zld) + zld;
+}
+inline size_t fwd_workspace_bytes(int B, int T, int nx, int nu, int elem, bool diag) {
+  return 256 + fwd_gain_bytes(B, T, nx, nu, elem) + (size_t)B * T * fwd_rec_elems(nx, nu, elem, diag) * elem;
 }
 
 template <class M, int G, bool DIAG, class R>
@@ -75,13 +94,36 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   a.converged = io->converged; a.diverged = io->diverged; a.fail_t = io->fail_t;
   a.clamped = io->clamped; a.alpha_hist = io->alpha_hist; a.J_hist = io->J_hist;
   auto kern = ilqr_forward_kernel<M, G, DIAG, R>;
-  if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
+  int per_sm = 1;
+  if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)) return -1;
+  if (p->B < a.gpb) {  // small batch: one block of the next power of two >= B groups
+    int g = 1;
+    while (g < p->B) g *= 2;
+    a.gpb = g;
+  }
+  a.pw = (32 / G < a.gpb) ? 32 / G : a.gpb;
   const int smem = a.gpb * a.smem_stride;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int blocks = (p->B + a.gpb - 1) / a.gpb;
+  // persistent grid: at most the resident blocks; warps claim problems dynamically
+  const int need_blocks = (p->B + a.gpb - 1) / a.gpb;
+  const int resident = per_sm * num_sms();
+  const int blocks = need_blocks < resident ? need_blocks : resident;
+  // workspace (caller-provided, else stream-ordered pool allocation)
+  const size_t wsb = fwd_workspace_bytes(p->B, p->T, M::NX, M::NU, (int)sizeof(R), DIAG);
+  void* ws = io->workspace;
+  bool own = false;
+  if (!ws || io->workspace_bytes < wsb) {
+    if (cudaMallocAsync(&ws, wsb, s) != cudaSuccess) return fail("forward: workspace allocation of %zu bytes failed", wsb);
+    own = true;
+  }
+  a.ctr = (int*)ws;
+  a.Kw = (unsigned char*)ws + 256;
+  a.Pw = (unsigned char*)ws + 256 + fwd_gain_bytes(p->B, p->T, M::NX, M::NU, (int)sizeof(R));
+  cudaMemsetAsync(ws, 0, sizeof(int), s);
   kern<<<blocks, a.gpb * G, smem, s>>>(a);
   g_launches.fetch_add(1);
   cudaError_t e = cudaGetLastError();
+  if (own) cudaFreeAsync(ws, s);
   if (e != cudaSuccess) return fail("forward launch failed: %s", cudaGetErrorString(e));
   return 0;
 }

@@ -72,7 +72,7 @@ struct Dims {
 template <class M, bool DIAG, class R>
 struct RicLayout {
   using D = Dims<M, DIAG, R>;
-  int oAs, oBs, oMA, oNB, oKT, oQuxT, oQuuKT, oQuu, oqu, oVx, ozs, oC, oc, end;
+  int oAs, oBs, oMA, oNB, oKT, oQuu, oqu, oVx, ozs, oC, oc, end;
   __host__ __device__ static RicLayout make(int o) {
     RicLayout L;
     const int s = (int)sizeof(R);
@@ -82,8 +82,6 @@ struct RicLayout {
     L.oMA = take(D::NX * D::LDA);
     L.oNB = take(D::NX * D::LDB);
     L.oKT = take(D::NX * D::LDB);
-    L.oQuxT = take(D::NX * D::LDB);
-    L.oQuuKT = take(D::NX * D::LDB);
     L.oQuu = take(D::NU * D::LDB);
     L.oqu = take(D::LDB);
     L.oVx = take(D::LDA);
@@ -98,11 +96,13 @@ struct RicLayout {
 template <class M, bool DIAG, class R>
 struct Ric {
   using D = Dims<M, DIAG, R>;
-  R *As, *Bs, *MA, *NB, *KT, *QuxT, *QuuKT, *Quu, *qu, *Vx, *zs, *Cb, *cb;
+  // QuxT (the Q_ux columns, full value update only) aliases NB, which is dead once the
+  // Q_uu entries are formed.
+  R *As, *Bs, *MA, *NB, *KT, *QuxT, *Quu, *qu, *Vx, *zs, *Cb, *cb;
   DMPC_DEV void bind(unsigned char* base, const RicLayout<M, DIAG, R>& L) {
     As = (R*)(base + L.oAs); Bs = (R*)(base + L.oBs); MA = (R*)(base + L.oMA);
-    NB = (R*)(base + L.oNB); KT = (R*)(base + L.oKT); QuxT = (R*)(base + L.oQuxT);
-    QuuKT = (R*)(base + L.oQuuKT); Quu = (R*)(base + L.oQuu); qu = (R*)(base + L.oqu);
+    NB = (R*)(base + L.oNB); KT = (R*)(base + L.oKT); QuxT = NB;
+    Quu = (R*)(base + L.oQuu); qu = (R*)(base + L.oqu);
     Vx = (R*)(base + L.oVx); zs = (R*)(base + L.ozs); Cb = (R*)(base + L.oC); cb = (R*)(base + L.oc);
   }
 };
@@ -140,27 +140,53 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
     R* d2 = S.cb + buf * D::ZLD;
     for (int e = lane; e < D::NZ; e += G) cp_async_elem(d2 + e, s2 + e);
   }
-  cp_async_commit();
 }
 
 // Software pipeline over the per-stage cost tensors: `acquire(t)` makes C_t resident
 // (issuing the prefetch of the next stage first when double-buffered); `release(t)`
 // is called once every lane is done with C_t and, when single-buffered, issues the
 // prefetch of the next stage into the same buffer. `step` is the traversal
-// direction (-1 backward sweeps, +1 forward rollouts).
+// direction (-1 backward sweeps, +1 forward rollouts). With `Kg` set, the stage's
+// feedback gains K_t (NU padded rows, written by this group's Riccati sweep into the
+// L2-resident gain workspace) ride along as 16-byte cp.async.cg copies into `Kb`.
 template <class M, bool DIAG, class R, int G>
 struct CostPipe {
   using D = Dims<M, DIAG, R>;
+  static constexpr int KCH = D::NU * D::LDA * (int)sizeof(R) / 16;  // 16-byte chunks of K_t
   const Ric<M, DIAG, R>* S;
   const R* Cg;
   const R* cg;
   int T, lane, step;
+  const R* Kg = nullptr;  // gain workspace of this problem, [t][NU][LDA]
+  R* Kb = nullptr;        // NBUF smem buffers of NU*LDA
+  const R* Pk = nullptr;  // packed stage records [C_t padded rows | c_t padded] (REC elements)
+  static constexpr int REC = D::NCSP + D::ZLD;
+  static constexpr int CCH = D::NCSP * (int)sizeof(R) / 16, cCH = D::ZLD * (int)sizeof(R) / 16;
   DMPC_DEV int buf(int t) const { return D::NBUF == 2 ? (t & 1) : 0; }
-  DMPC_DEV void start(int t0) { stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, t0, buf(t0), lane); }
+  DMPC_DEV void issue(int t) {
+    if (Pk) {  // one 16-byte cp.async per chunk, no index remapping
+      const char* src = (const char*)(Pk + (size_t)t * REC);
+      char* dc = (char*)(S->Cb + buf(t) * D::NCSP);
+      char* dcc = (char*)(S->cb + buf(t) * D::ZLD);
+      for (int e = lane; e < CCH + cCH; e += G) {
+        if (e < CCH) cp_async_16cg(dc + 16 * e, src + 16 * e);
+        else cp_async_16cg(dcc + 16 * (e - CCH), src + 16 * e);
+      }
+    } else {
+      stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, t, buf(t), lane);
+    }
+    if (Kg) {
+      const char* src = (const char*)(Kg + (size_t)t * D::NU * D::LDA);
+      char* dst = (char*)(Kb + buf(t) * D::NU * D::LDA);
+      for (int e = lane; e < KCH; e += G) cp_async_16cg(dst + 16 * e, src + 16 * e);
+    }
+    cp_async_commit();
+  }
+  DMPC_DEV void start(int t0) { issue(t0); }
   DMPC_DEV void acquire(int t) {
     const int tn = t + step;
     if (D::NBUF == 2 && tn >= 0 && tn < T) {
-      stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, tn, buf(tn), lane);
+      issue(tn);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
       cp_async_wait_all();
@@ -168,10 +194,19 @@ struct CostPipe {
   }
   DMPC_DEV void release(int t) {
     const int tn = t + step;
-    if (D::NBUF == 1 && tn >= 0 && tn < T) stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, tn, 0, lane);
+    if (D::NBUF == 1 && tn >= 0 && tn < T) issue(tn);
+  }
+  // write the resident (padded) C_t / c_t out as packed record t (16-byte stores); later
+  // sweeps stage it back with plain 16-byte copies
+  DMPC_DEV void pack_out(R* dst, int t) const {
+    const uint4* sc = (const uint4*)(S->Cb + buf(t) * D::NCSP);
+    const uint4* scc = (const uint4*)(S->cb + buf(t) * D::ZLD);
+    uint4* d = (uint4*)(dst + (size_t)t * REC);
+    for (int e = lane; e < CCH + cCH; e += G) d[e] = e < CCH ? sc[e] : scc[e - CCH];
   }
   DMPC_DEV const R* C(int t) const { return S->Cb + buf(t) * D::NCSP; }
   DMPC_DEV const R* c(int t) const { return S->cb + buf(t) * D::ZLD; }
+  DMPC_DEV const R* K(int t) const { return Kb + buf(t) * D::NU * D::LDA; }
 };
 
 // ---------------------------------------------------------------------------
@@ -294,36 +329,64 @@ DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j) {
   return s;
 }
 
-// Publish column a of K, Qux and Quu K for the value-Hessian update.
+// Publish column a of K (and, for the full value update, of Qux).
 template <class M, bool DIAG, class R>
 DMPC_DEV void ric_publish_cols(const Ric<M, DIAG, R>& S, int a, const R (&kcol)[M::NU], const R (&quxc)[M::NU],
-                               const R (&quu)[M::NU][M::NU]) {
+                               bool lean) {
   using D = Dims<M, DIAG, R>;
   constexpr int NU = M::NU;
 #pragma unroll
-  for (int i = 0; i < NU; i++) {
-    S.KT[a * D::LDB + i] = kcol[i];
-    S.QuxT[a * D::LDB + i] = quxc[i];
-    R s = R(0);
+  for (int i = 0; i < NU; i++) S.KT[a * D::LDB + i] = kcol[i];
+  if (lean) return;
 #pragma unroll
-    for (int q = 0; q < NU; q++) s += quu[i][q] * kcol[q];
-    S.QuuKT[a * D::LDB + i] = s;
-  }
+  for (int i = 0; i < NU; i++) S.QuxT[a * D::LDB + i] = quxc[i];
 }
 
-// newVxx rows -> N (aliases MA): s = Qxx[a,b] + sum_r (K_ra QuuK_rb + K_ra Qux_rb) + Qux_ra K_rb
-// (kernels.py:499-507)
+// newVxx rows -> N (aliases MA) (kernels.py:499-507):
+//   full:  N[a,b] = Qxx[a,b] + sum_r (K_ra (Quu K)_rb + K_ra Qux_rb) + Qux_ra K_rb
+//   lean:  N[a,b] = Qxx[a,b] + sum_r Qux_ra K_rb
+// The lean form is exact whenever K = -Quu_ff^-1 Qux_f on the free rows and zero on the
+// clamped ones with the SAME Quu the update uses (lambda = 0 in the primal sweep; always in
+// the auxiliary sweep, whose Quu is the frozen one it factorises): then
+// K'Quu K = -K'Qux and the first two terms cancel. The full form (lambda > 0, rare)
+// recomputes the column (Quu K)[:,b] from the published K column.
 template <class M, bool DIAG, class R, int G, int RPL>
 DMPC_DEV void ric_Vxx_rows(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RPL][M::NX],
-                           const R (&kcol)[RPL][M::NU], const R (&quxc)[RPL][M::NU]) {
+                           const R (&kcol)[RPL][M::NU], const R (&quxc)[RPL][M::NU],
+                           const R (&quu)[M::NU][M::NU], bool lean) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
+  if (lean) {
+#pragma unroll
+    for (int bb = 0; bb < NX; bb++) {
+      R kk[NU];
+      lds_row<NU>(S.KT + bb * D::LDB, kk);
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int a = row_of<G, RPL>(lane, k);
+        R s0 = qxx[k][bb], s1 = R(0);
+#pragma unroll
+        for (int r = 0; r < NU; r += 2) {
+          s0 += quxc[k][r] * kk[r];
+          if (r + 1 < NU) s1 += quxc[k][r + 1] * kk[r + 1];
+        }
+        if (a < NX) S.MA[a * D::LDA + bb] = s0 + s1;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int bb = 0; bb < NX; bb++) {
-    R kq[NU], qx[NU], kk[NU];
-    lds_row<NU>(S.QuuKT + bb * D::LDB, kq);
+    R kk[NU], qx[NU], kq[NU];
     lds_row<NU>(S.QuxT + bb * D::LDB, qx);
     lds_row<NU>(S.KT + bb * D::LDB, kk);
+#pragma unroll
+    for (int r = 0; r < NU; r++) {
+      R t = R(0);
+#pragma unroll
+      for (int q = 0; q < NU; q++) t += quu[r][q] * kk[q];
+      kq[r] = t;
+    }
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
       const int a = row_of<G, RPL>(lane, k);

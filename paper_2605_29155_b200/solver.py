@@ -155,7 +155,12 @@ def solve_raw(model, settings, x_init, C, c, U_warm, *, dtype=torch.float32, dev
     for name in ("X", "U", "J", "K", "k", "iters", "converged", "diverged", "fail_t", "clamped",
                  "alpha_hist", "J_hist"):
         setattr(io, name, P(getattr(out, name)))
-    fn = getattr(_lib.lib(), f"diffmpc_forward_{_DT[dtype]}")
+    # device workspace (work counter + L2-resident gains) from torch's caching allocator
+    L = _lib.lib()
+    wsb = int(L.diffmpc_forward_workspace_bytes(ctypes.byref(p), 4 if dtype == torch.float32 else 8))
+    ws = torch.empty((wsb,), dtype=torch.uint8, device=dev)
+    io.workspace, io.workspace_bytes = P(ws), wsb
+    fn = getattr(L, f"diffmpc_forward_{_DT[dtype]}")
     with torch.cuda.device(dev):
         _lib.check(fn(ctypes.byref(p), ctypes.byref(io), _stream(stream)))
     out.converged = out.converged.bool()

@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "diffmpc.h")
 
 def declared_functions():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|int32_t|const char\*)\s+(diffmpc_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|int32_t|uint64_t|const char\*)\s+(diffmpc_\w+)\s*\(", txt, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

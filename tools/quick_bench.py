@@ -15,14 +15,14 @@ def run(kind_model, B, T, dtype, layout, reps=10, conv_tol=1e-6):
         out = solver.solve_raw(pb.model, pb.settings, x0, Ct, c, Uw, dtype=dtype)
         g = solver.backward_raw(pb.model, pb.settings, Ct, c, out.X, out.U, None, dLdU, dtype=dtype)
     torch.cuda.synchronize()
-    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-    tf = tb = 0.0
-    for _ in range(reps):
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
+    for e0, e1, e2 in ev:  # no per-rep sync: host overhead stays off the device timeline
         e0.record(); out = solver.solve_raw(pb.model, pb.settings, x0, Ct, c, Uw, dtype=dtype)
         e1.record(); g = solver.backward_raw(pb.model, pb.settings, Ct, c, out.X, out.U, None, dLdU, dtype=dtype)
-        e2.record(); torch.cuda.synchronize()
-        tf += e0.elapsed_time(e1); tb += e1.elapsed_time(e2)
-    tf /= reps; tb /= reps
+        e2.record()
+    torch.cuda.synchronize()
+    tf = sum(a.elapsed_time(b) for a, b, _ in ev) / reps
+    tb = sum(b.elapsed_time(c) for _, b, c in ev) / reps
     it = out.iters.float().mean().item()
     print(f"{'quad13' if kind_model.n_x==13 else 'planar'} B={B} T={T} {str(dtype)[6:]} {layout}: fwd {tf:.3f} ms  bwd {tb:.3f} ms  "
           f"mean iters {it:.2f}  -> {B/((tf+tb)*1e-3)/1e6:.2f} M solves/s", flush=True)
