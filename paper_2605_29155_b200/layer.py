@@ -101,9 +101,10 @@ class MpcSolveLayer(torch.autograd.Function):
             stats_sink.setdefault("solves", 0)
             stats_sink.setdefault("non_converged", 0)
             stats_sink.setdefault("iterations", 0)
+            # device-side counters (no host sync per solve); int() them when reading
             stats_sink["solves"] += ws.B
-            stats_sink["non_converged"] += int((~converged).sum().item())
-            stats_sink["iterations"] += int(iterations.sum().item())
+            stats_sink["non_converged"] = stats_sink["non_converged"] + (~converged).sum()
+            stats_sink["iterations"] = stats_sink["iterations"] + iterations.sum()
         return ws.U[:, 0].to(device=diag.device, dtype=diag.dtype)
 
     @staticmethod

@@ -1,0 +1,148 @@
+"""PPO plumbing around the DiffMPC layer.
+
+CPU: gae against a loop restatement of trainer.py:66-91, and the world_size-2 gloo path
+of the data-parallel update (one flat gradient all-reduce per minibatch) against a
+single-process update on the full minibatch, in the solver-free ac_mlp mode.
+GPU: the ac_mpc minibatch step through the B200 layer (ratio 1 at the trust-region
+centre, gradients reach the cost actor)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2605_29155_b200 import DynModel, SolveSettings
+from paper_2605_29155_b200.policy import CostHeadScaling, PolicyBundle
+from paper_2605_29155_b200 import ppo
+
+
+def _gae_ref(rewards, values, dones, gamma, lam, last_values):
+    S = rewards.shape[0]
+    adv = np.zeros_like(rewards)
+    next_adv = np.zeros_like(last_values)
+    next_val = last_values
+    for s in range(S - 1, -1, -1):
+        nt = 1.0 - dones[s]
+        delta = rewards[s] + gamma * next_val * nt - values[s]
+        next_adv = delta + gamma * lam * nt * next_adv
+        adv[s] = next_adv
+        next_val = values[s]
+    return adv, adv + values
+
+
+def test_gae_matches_loop_restatement():
+    rng = np.random.default_rng(0)
+    r, v = rng.normal(size=(7, 5)), rng.normal(size=(7, 5))
+    d = (rng.random((7, 5)) < 0.2).astype(float)
+    lv = rng.normal(size=5)
+    a, ret = ppo.gae(r, v, d, 0.99, 0.95, lv)
+    a2, ret2 = _gae_ref(r, v, d, 0.99, 0.95, lv)
+    np.testing.assert_array_equal(a.numpy(), a2)
+    np.testing.assert_array_equal(ret.numpy(), ret2)
+
+
+def _bundle(mode="ac_mlp", seed=0):
+    torch.manual_seed(seed)
+    model = DynModel.quadrotor(dt=0.05)
+    st = SolveSettings(T=4, u_min=0.0, u_max=model.params[0] * model.params[-1])
+    return PolicyBundle(mode, 13, model, st, CostHeadScaling.for_model(model, 13), hidden=(32, 32)), model, st
+
+
+def _buffer(n, model, T, seed=1):
+    g = torch.Generator().manual_seed(seed)
+    return {"obs": torch.randn(n, 13, generator=g), "actions": torch.rand(n, 4, generator=g) * 5,
+            "log_probs": torch.randn(n, generator=g) - 3, "advantages": torch.randn(n, generator=g),
+            "returns": torch.randn(n, generator=g)}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, model, st = _bundle()
+    cfg = ppo.TrainConfig(mode="ac_mlp", minibatch_size=64, sgd_epochs=2, normalize_advantages=False)
+    opt = torch.optim.Adam(b.parameters(), lr=1e-3)
+    red = ppo.GradAllReduce(b.parameters())
+    ppo.ppo_update(_buffer(128, model, st.T), b, opt, cfg, generator=torch.Generator().manual_seed(3),
+                   reducer=red, rank=rank, world=world)
+    flat = torch.cat([p.detach().reshape(-1) for p in b.parameters()])
+    parts = [torch.empty_like(flat) for _ in range(world)]
+    dist.all_gather(parts, flat)
+    if rank == 0:
+        q.put((parts[0].numpy(), parts[1].numpy(), red.nbytes))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_data_parallel_update_matches_single_process():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    p0, p1, nbytes = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    np.testing.assert_array_equal(p0, p1)  # replicas stay identical
+    # single process, full minibatches: the mean of the two shard means is the full mean
+    b, model, st = _bundle()
+    cfg = ppo.TrainConfig(mode="ac_mlp", minibatch_size=64, sgd_epochs=2, normalize_advantages=False)
+    opt = torch.optim.Adam(b.parameters(), lr=1e-3)
+    ppo.ppo_update(_buffer(128, model, st.T), b, opt, cfg, generator=torch.Generator().manual_seed(3))
+    ref = torch.cat([p.detach().reshape(-1) for p in b.parameters()]).numpy()
+    np.testing.assert_allclose(p0, ref, rtol=1e-5, atol=1e-6)
+    assert nbytes == 4 * sum(p.numel() for p in b.parameters())
+
+
+def test_ac_mpc_bundle_sizes_match_reference_formula():
+    """Actor head T*2*n_z and the flat bucket size quoted in SURVEY.md §8(e)."""
+    model = DynModel.quadrotor(dt=0.05)
+    st = SolveSettings(T=10, u_min=0.0, u_max=5.886)
+    b = PolicyBundle("ac_mpc", 11, model, st, CostHeadScaling.for_model(model, 13))
+    assert b.actor.net[-1].out_features == 10 * 2 * 17
+    n = sum(p.numel() for p in b.parameters())
+    assert n == (11 * 512 + 512 + 512 * 512 + 512 + 512 * 340 + 340) + (11 * 512 + 512 + 512 * 512 + 512 + 513) + 4
+
+
+@pytest.mark.gpu
+def test_ac_mpc_minibatch_step_on_gpu():
+    from paper_2605_29155_b200 import problems
+    from paper_2605_29155_b200.layer import MpcSolver, mpc_control
+
+    dev = torch.device("cuda")
+    model = DynModel.quadrotor(dt=0.05)
+    pb = problems.hover_problem(model, 256, 10, seed=4)
+    b, _, _ = _bundle("ac_mpc")
+    b = PolicyBundle("ac_mpc", 13, model, pb.settings, CostHeadScaling.for_model(model, 13), hidden=(64, 64)).to(dev)
+    solver = MpcSolver(model, pb.settings, device=dev)
+    obs = torch.tensor(pb.x0, dtype=torch.float32, device=dev)
+    x_init = torch.tensor(pb.x0, dtype=torch.float32, device=dev)
+    U_warm = torch.tensor(pb.U_warm, dtype=torch.float32, device=dev)
+    with torch.no_grad():
+        u_mean = mpc_control(b, obs, solver, x_init, U_warm)
+        sig = torch.exp(b.log_sigma)
+        actions = u_mean + sig * torch.randn_like(u_mean)
+        lp = torch.distributions.Normal(u_mean, sig).log_prob(actions).sum(-1)
+    batch = {"obs": obs, "actions": actions, "old_log_probs": lp, "advantages": torch.randn(256, device=dev),
+             "returns": torch.randn(256, device=dev), "x_init": x_init, "U_warm": U_warm}
+    cfg = ppo.TrainConfig()
+    loss, metrics = ppo.ppo_losses(b, batch, cfg, solver)
+    assert abs(float(metrics["mean_ratio"]) - 1.0) < 1e-6  # exact re-solve: ratio 1
+    opt = torch.optim.Adam(b.parameters(), lr=1e-4)
+    before = [p.detach().clone() for p in b.actor.parameters()]
+    loss, _ = ppo.minibatch_step(b, opt, batch, cfg, solver, reducer=ppo.GradAllReduce(b.parameters()))
+    assert loss is not None and torch.isfinite(loss)
+    moved = sum(float((p.detach() - q).abs().sum()) for p, q in zip(b.actor.parameters(), before))
+    assert moved > 0.0  # the cost actor is trained through the DiffMPC layer
