@@ -343,24 +343,24 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       const R* Cs = bwdp.C(t);
       const R* cs = bwdp.c(t);
       // nominal point, state-dependent Jacobian entries
-      double xd[NX], ud[NU];
-      lds_row_d<NX>(Xn + t * XLD, xd);
+      double ud[NU];
       lds_row_d<NU>(Un + t * ULD, ud);
-      R xr[NX], ur[NU];
+      // z_t in the Riccati type: entry i converted once, by lane i (mod G)
+      for (int i = lane; i < NZ; i += G) S.zs[i] = (R)(i < NX ? Xn[t * XLD + i] : Un[t * ULD + i - NX]);
+      __syncwarp(gm);  // previous stage done with As/Bs/MA; z_t and the staging visible
+      R zv[NZ], vx[NX];
+      lds_row<NZ>(S.zs, zv);
+      if constexpr (!M::kLinearParams) {
+        R xr[NX], ur[NU];
 #pragma unroll
-      for (int i = 0; i < NX; i++) xr[i] = (R)xd[i];
+        for (int i = 0; i < NX; i++) xr[i] = zv[i];
 #pragma unroll
-      for (int i = 0; i < NU; i++) ur[i] = (R)ud[i];
-      __syncwarp(gm);  // previous stage done with As/Bs/MA; staging visible
-      if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
-#pragma unroll
-      for (int i = 0; i < NZ; i++)
-        if ((i % G) == lane) S.zs[i] = (i < NX) ? xr[i < NX ? i : 0] : ur[i >= NX ? i - NX : 0];
+        for (int i = 0; i < NU; i++) ur[i] = zv[NX + i];
+        M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
+      }
       __syncwarp(gm);
       // gz = C z + c ; qx = gz_x + A' Vx ; qu = gz_u + B' Vx   (kernels.py:395-410)
       R qx[RPL];
-      R zv[NZ], vx[NX];
-      lds_row<NZ>(S.zs, zv);
       lds_row<NX>(S.Vx, vx);
 #pragma unroll
       for (int k = 0; k < RPL; k++) {
