@@ -473,13 +473,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     const int slot = lane / LC, j = lane % LC;
     const unsigned smask = (LC == 32) ? 0xffffffffu
                                       : (((1u << LC) - 1u) << ((threadIdx.x & 31u) & ~(unsigned)(LC - 1)));
-    double Jc[8];
-    bool dead[8];
-#pragma unroll
-    for (int a = 0; a < 8; a++) {
-      Jc[a] = 0.0;
-      dead[a] = false;
-    }
+    // candidates are folded in increasing alpha index as they complete: the first
+    // minimum wins ties (argmin, ilqr.py:218-222)
+    double best_J = 0.0;
+    int best = 0;
+    bool alld = false;
     const bool inplace = args.n_alpha <= NSLOT;  // one round: alpha_0 may overwrite X
     if (active) {
       const int NA = args.n_alpha;
@@ -552,12 +550,20 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         for (int s = 0; s < NSLOT; s++) {
           const double Js = __shfl_sync(gm, Jm, s * LC, G);
           const bool ds = __shfl_sync(gm, (int)dm, s * LC, G) != 0;
-#pragma unroll
-          for (int a = 0; a < 8; a++)
-            if (a == round * NSLOT + s && a < NA) {
-              Jc[a] = Js;
-              dead[a] = ds;
+          const int a = round * NSLOT + s;
+          if (a < NA) {
+            if (a == 0) {
+              best_J = Js;
+              best = 0;
+              alld = ds;
+            } else {
+              if (Js < best_J) {
+                best_J = Js;
+                best = a;
+              }
+              alld = alld && ds;
             }
+          }
         }
         __syncwarp(gm);
       }
@@ -566,19 +572,6 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     // ------------------------- epilogue (ilqr.py:216-244) -----------------------
     const int act = active;
     if (act) iterations = it + 1;
-    int best = 0;
-    double best_J = Jc[0];
-    bool alld = dead[0];
-#pragma unroll
-    for (int a = 1; a < 8; a++) {
-      if (a < args.n_alpha) {
-        if (Jc[a] < best_J) {
-          best_J = Jc[a];
-          best = a;
-        }
-        alld = alld && dead[a];
-      }
-    }
     const bool all_dead = act && alld;
     const bool accept = act && !all_dead && (best_J < J);
     if (ahist && lane == 0) ahist[it] = accept ? (R)args.alphas[best] : R(0);
