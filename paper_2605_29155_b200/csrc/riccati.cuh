@@ -64,6 +64,7 @@ struct Dims {
   static constexpr int NCSP = DIAG ? ZLD : NZ * ZLD;  // staged C_t (padded rows)
   static constexpr int NBUF = DIAG ? 2 : 1;            // staging buffers (dense: 1 to save smem)
   static constexpr int NCS = DIAG ? NZ : NZ * NZ;     // C_t in global memory
+  static constexpr int REC = NCSP + ZLD;               // stage record [C_t padded | c_t padded]
   static constexpr int XLD = rup(NX, 2);   // rows of the double trajectories
   static constexpr int ULD = rup(NU, 2);
 };
@@ -72,7 +73,7 @@ struct Dims {
 template <class M, bool DIAG, class R>
 struct RicLayout {
   using D = Dims<M, DIAG, R>;
-  int oAs, oBs, oMA, oNB, oKT, oQuu, oqu, oVx, ozs, oC, oc, end;
+  int oAs, oBs, oMA, oNB, oKT, oQuu, oqu, oVx, ozs, oR, end;
   __host__ __device__ static RicLayout make(int o) {
     RicLayout L;
     const int s = (int)sizeof(R);
@@ -86,8 +87,7 @@ struct RicLayout {
     L.oqu = take(D::LDB);
     L.oVx = take(D::LDA);
     L.ozs = take(D::ZLD);
-    L.oC = take(D::NBUF * D::NCSP);
-    L.oc = take(D::NBUF * D::ZLD);
+    L.oR = take(D::NBUF * D::REC);  // NBUF contiguous stage records
     L.end = o;
     return L;
   }
@@ -98,12 +98,14 @@ struct Ric {
   using D = Dims<M, DIAG, R>;
   // QuxT (the Q_ux columns, full value update only) aliases NB, which is dead once the
   // Q_uu entries are formed.
-  R *As, *Bs, *MA, *NB, *KT, *QuxT, *Quu, *qu, *Vx, *zs, *Cb, *cb;
+  R *As, *Bs, *MA, *NB, *KT, *QuxT, *Quu, *qu, *Vx, *zs, *Rb;
+  DMPC_DEV R* Cb(int b) const { return Rb + b * D::REC; }
+  DMPC_DEV R* cb(int b) const { return Rb + b * D::REC + D::NCSP; }
   DMPC_DEV void bind(unsigned char* base, const RicLayout<M, DIAG, R>& L) {
     As = (R*)(base + L.oAs); Bs = (R*)(base + L.oBs); MA = (R*)(base + L.oMA);
     NB = (R*)(base + L.oNB); KT = (R*)(base + L.oKT); QuxT = NB;
     Quu = (R*)(base + L.oQuu); qu = (R*)(base + L.oqu);
-    Vx = (R*)(base + L.oVx); zs = (R*)(base + L.ozs); Cb = (R*)(base + L.oC); cb = (R*)(base + L.oc);
+    Vx = (R*)(base + L.oVx); zs = (R*)(base + L.ozs); Rb = (R*)(base + L.oR);
   }
 };
 
@@ -112,7 +114,7 @@ template <class M, bool DIAG, class R, int G>
 DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, int t, int buf, int lane) {
   using D = Dims<M, DIAG, R>;
   const R* src = Cg + (size_t)t * D::NCS;
-  R* dst = S.Cb + buf * D::NCSP;
+  R* dst = S.Cb(buf);
   if constexpr (DIAG) {
     for (int e = lane; e < D::NZ; e += G) cp_async_elem(dst + e, src + e);
   } else {
@@ -137,7 +139,7 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
   }
   if (cg) {
     const R* s2 = cg + (size_t)t * D::NZ;
-    R* d2 = S.cb + buf * D::ZLD;
+    R* d2 = S.cb(buf);
     for (int e = lane; e < D::NZ; e += G) cp_async_elem(d2 + e, s2 + e);
   }
 }
@@ -160,25 +162,25 @@ struct CostPipe {
   const R* Kg = nullptr;  // gain workspace of this problem, [t][NU][LDA]
   R* Kb = nullptr;        // NBUF smem buffers of NU*LDA
   const R* Pk = nullptr;  // packed stage records [C_t padded rows | c_t padded] (REC elements)
-  static constexpr int REC = D::NCSP + D::ZLD;
-  static constexpr int CCH = D::NCSP * (int)sizeof(R) / 16, cCH = D::ZLD * (int)sizeof(R) / 16;
+  static constexpr int REC = D::REC;
+  static constexpr int NCH = REC * (int)sizeof(R) / 16;  // 16-byte chunks per record
   DMPC_DEV int buf(int t) const { return D::NBUF == 2 ? (t & 1) : 0; }
   DMPC_DEV void issue(int t) {
-    if (Pk) {  // one 16-byte cp.async per chunk, no index remapping
-      const char* src = (const char*)(Pk + (size_t)t * REC);
-      char* dc = (char*)(S->Cb + buf(t) * D::NCSP);
-      char* dcc = (char*)(S->cb + buf(t) * D::ZLD);
-      for (int e = lane; e < CCH + cCH; e += G) {
-        if (e < CCH) cp_async_16cg(dc + 16 * e, src + 16 * e);
-        else cp_async_16cg(dcc + 16 * (e - CCH), src + 16 * e);
-      }
+    if (Pk) {  // contiguous record -> contiguous buffer: fully unrolled 16-byte copies
+      const char* src = (const char*)(Pk + (size_t)t * REC) + 16 * lane;
+      char* dst = (char*)S->Cb(buf(t)) + 16 * lane;
+#pragma unroll
+      for (int k = 0; k < (NCH + G - 1) / G; k++)
+        if (k * G + lane < NCH) cp_async_16cg(dst + 16 * G * k, src + 16 * G * k);
     } else {
       stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, t, buf(t), lane);
     }
     if (Kg) {
-      const char* src = (const char*)(Kg + (size_t)t * D::NU * D::LDA);
-      char* dst = (char*)(Kb + buf(t) * D::NU * D::LDA);
-      for (int e = lane; e < KCH; e += G) cp_async_16cg(dst + 16 * e, src + 16 * e);
+      const char* src = (const char*)(Kg + (size_t)t * D::NU * D::LDA) + 16 * lane;
+      char* dst = (char*)(Kb + buf(t) * D::NU * D::LDA) + 16 * lane;
+#pragma unroll
+      for (int k = 0; k < (KCH + G - 1) / G; k++)
+        if (k * G + lane < KCH) cp_async_16cg(dst + 16 * G * k, src + 16 * G * k);
     }
     cp_async_commit();
   }
@@ -199,13 +201,14 @@ struct CostPipe {
   // write the resident (padded) C_t / c_t out as packed record t (16-byte stores); later
   // sweeps stage it back with plain 16-byte copies
   DMPC_DEV void pack_out(R* dst, int t) const {
-    const uint4* sc = (const uint4*)(S->Cb + buf(t) * D::NCSP);
-    const uint4* scc = (const uint4*)(S->cb + buf(t) * D::ZLD);
-    uint4* d = (uint4*)(dst + (size_t)t * REC);
-    for (int e = lane; e < CCH + cCH; e += G) d[e] = e < CCH ? sc[e] : scc[e - CCH];
+    const uint4* sr = (const uint4*)S->Cb(buf(t)) + lane;
+    uint4* d = (uint4*)(dst + (size_t)t * REC) + lane;
+#pragma unroll
+    for (int k = 0; k < (NCH + G - 1) / G; k++)
+      if (k * G + lane < NCH) d[G * k] = sr[G * k];
   }
-  DMPC_DEV const R* C(int t) const { return S->Cb + buf(t) * D::NCSP; }
-  DMPC_DEV const R* c(int t) const { return S->cb + buf(t) * D::ZLD; }
+  DMPC_DEV const R* C(int t) const { return S->Cb(buf(t)); }
+  DMPC_DEV const R* c(int t) const { return S->cb(buf(t)); }
   DMPC_DEV const R* K(int t) const { return Kb + buf(t) * D::NU * D::LDA; }
 };
 
