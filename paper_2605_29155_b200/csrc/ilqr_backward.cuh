@@ -310,27 +310,48 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         }
       }
       // assembly of stage t: dc = dz, dC = 0.5 (dz z' + z dz'), clamped rows/cols zero;
-      // plus the optimal-cost terms sJ z and sJ/2 z z'
-      auto zat = [&](int a) -> R { return a < NX ? Xs[t * LDA + a] : Us[t * LDB + a - NX]; };
-      auto dzat = [&](int a) -> R { return a < NX ? dXs[t * LDA + a] : dUs[t * LDB + a - NX]; };
-      auto clat = [&](int a) -> bool { return a >= NX && cl[t * NU + a - NX]; };
-      if (dco) {
-        for (int a = lane; a < NZ; a += G) dco[t * NZ + a] = (clat(a) ? R(0) : dzat(a)) + sJ * zat(a);
-      }
-      if (dCo) {
-        if constexpr (DIAG) {
-          for (int a = lane; a < NZ; a += G) {
-            const R za = zat(a), da = dzat(a);
-            const R v = clat(a) ? R(0) : R(0.5) * (da * za + za * da);
-            dCo[t * NZ + a] = v + R(0.5) * sJ * za * za;
-          }
-        } else {
-          for (int e = lane; e < NZ * NZ; e += G) {
-            const int a = e / NZ, b = e % NZ;
-            const R za = zat(a), zb = zat(b);
-            // products rounded separately (no FMA contraction) so dC is exactly symmetric
-            const R v = (clat(a) || clat(b)) ? R(0) : R(0.5) * (mul_rn(dzat(a), zb) + mul_rn(za, dzat(b)));
-            dCo[(size_t)t * NZ * NZ + e] = v + R(0.5) * sJ * za * zb;
+      // plus the optimal-cost terms sJ z and sJ/2 z z'. Lane a owns row a (rows a + G for
+      // a < NZ - G): z, dz and the clamp mask are in registers with compile-time column
+      // indices, so each entry is a few FMAs and one store (no index arithmetic).
+      {
+        R zr[NZ], dzr[NZ];
+        bool clr[NZ];
+#pragma unroll
+        for (int i = 0; i < NX; i++) {
+          zr[i] = xr[i];
+          dzr[i] = dx[i];
+          clr[i] = false;
+        }
+#pragma unroll
+        for (int i = 0; i < NU; i++) {
+          zr[NX + i] = ur[i];
+          dzr[NX + i] = du[i];
+          clr[NX + i] = cl[t * NU + i] != 0;
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < (NZ + G - 1) / G; k2++) {
+          const int a = lane + k2 * G;
+          if (a < NZ) {
+            const bool isx = a < NX;
+            const R za = isx ? Xs[t * LDA + a] : Us[t * LDB + (isx ? 0 : a - NX)];
+            const R da = isx ? dXs[t * LDA + a] : dUs[t * LDB + (isx ? 0 : a - NX)];
+            const bool ca = !isx && cl[t * NU + (isx ? 0 : a - NX)] != 0;
+            if (dco) dco[t * NZ + a] = (ca ? R(0) : da) + sJ * za;
+            if (dCo) {
+              if constexpr (DIAG) {
+                const R v = ca ? R(0) : R(0.5) * (da * za + za * da);
+                dCo[t * NZ + a] = v + R(0.5) * sJ * za * za;
+              } else {
+                R* row = dCo + ((size_t)t * NZ + a) * NZ;
+                const R hs = R(0.5) * sJ * za;
+#pragma unroll
+                for (int b = 0; b < NZ; b++) {
+                  // products rounded separately (no FMA contraction) so dC is exactly symmetric
+                  const R v = (ca || clr[b]) ? R(0) : R(0.5) * (mul_rn(da, zr[b]) + mul_rn(za, dzr[b]));
+                  row[b] = v + hs * zr[b];
+                }
+              }
+            }
           }
         }
       }
