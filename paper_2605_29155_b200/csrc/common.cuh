@@ -34,6 +34,21 @@ DMPC_DEV void cp_async_elem(float* dst, const float* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
 }
+// Streaming variants: the caller's cost tensors are read once per stage, so their L2 lines
+// are marked evict-first (they must not push the resident per-problem workspace out).
+DMPC_DEV uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+DMPC_DEV void cp_async_elem(float* dst, const float* src, uint64_t pol) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "l"(pol));
+}
+DMPC_DEV void cp_async_elem(double* dst, const double* src, uint64_t pol) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "l"(pol));
+}
 DMPC_DEV void cp_async_elem(double* dst, const double* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
@@ -43,6 +58,12 @@ DMPC_DEV void cp_async_elem(double* dst, const double* src) {
 DMPC_DEV void cp_async_16cg(void* dst, const void* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+// Drop one 128-byte L2 line without writing it back (its contents become undefined):
+// used on the workspace of a finished problem, which is never read again.
+DMPC_DEV void l2_discard(const void* p) {
+  asm volatile("{\n\t.reg .u64 ga;\n\tcvta.to.global.u64 ga, %0;\n\tdiscard.global.L2 [ga], 128;\n\t}\n" ::"l"(p)
+               : "memory");
 }
 DMPC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 DMPC_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }

@@ -63,6 +63,7 @@ struct FwdArgs {
   void* J_hist;
   void* Kw;            // gain workspace (B, T, NU, LDA) of R
   void* Pw;            // packed cost records (B, T, REC) of R
+  long long kw_stride, pw_stride;  // per-problem workspace strides (elements of R, 128-byte multiples)
   int* ctr;            // per-launch work counter (zeroed before the launch)
   int pw;              // problems per warp claimed by one atomicAdd (32/G, or gpb if smaller)
 };
@@ -173,12 +174,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   double* Us = Ubuf1;
   const R* Cg = (const R*)args.C + (size_t)pid * T * D::NCS;
   const R* cg = (const R*)args.c + (size_t)pid * T * NZ;
-  R* Kw = (R*)args.Kw + (size_t)pid * T * NU * LDA;
+  R* Kw = (R*)args.Kw + (size_t)pid * args.kw_stride;
   R* Ko = args.K ? (R*)args.K + (size_t)pid * T * NU * NX : nullptr;
   // the initial rollout stages C_t / c_t element-wise from the caller's arrays and writes
   // them out as packed, 16-byte aligned records (Pw); every later sweep and line search
   // stages those with 16-byte copies
-  R* Pw = (R*)args.Pw + (size_t)pid * T * CostPipe<M, DIAG, R, G>::REC;
+  R* Pw = (R*)args.Pw + (size_t)pid * args.pw_stride;
   CostPipe<M, DIAG, R, G> fwdp{&S, Cg, cg, T, lane, +1};
   CostPipe<M, DIAG, R, G> bwdp{&S, Cg, cg, T, lane, -1, nullptr, nullptr, Pw};
   CostPipe<M, DIAG, R, G> lsp{&S, Cg, cg, T, lane, +1, Kw, Kb, Pw};
@@ -708,6 +709,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     }
   }
   __syncwarp(gm);
+  // the problem's gain / record lines are dead: drop them from L2 instead of writing back
+  for (int l = lane; l < (int)(args.kw_stride * sizeof(R) / 128); l += G) l2_discard((const char*)Kw + 128 * l);
+  for (int l = lane; l < (int)(args.pw_stride * sizeof(R) / 128); l += G) l2_discard((const char*)Pw + 128 * l);
   }  // pid < B
   }  // persistent loop
 }

@@ -60,18 +60,24 @@ int num_sms();
 
 // Forward workspace: [work counter (256 B)] [gains K (B, T, NU, LDA) of R]
 //                    [packed cost records (B, T, REC) of R]
-inline size_t fwd_gain_bytes(int B, int T, int nx, int nu, int elem) {
+inline size_t rup128(size_t v) { return (v + 127) / 128 * 128; }
+// per-problem strides (bytes), 128-byte multiples so a finished problem's lines can be
+// discarded from L2 without touching a neighbour's
+inline size_t fwd_gain_stride(int T, int nx, int nu, int elem) {
   const int vn = 16 / elem;
   const size_t lda = (size_t)((nx + vn - 1) / vn * vn);
-  return (size_t)B * T * nu * lda * elem;
+  return rup128((size_t)T * nu * lda * elem);
 }
 inline size_t fwd_rec_elems(int nx, int nu, int elem, bool diag) {
   const int vn = 16 / elem, nz = nx + nu;
   const size_t zld = (size_t)((nz + vn - 1) / vn * vn);
   return (diag ? zld : nz * zld) + zld;
 }
+inline size_t fwd_rec_stride(int T, int nx, int nu, int elem, bool diag) {
+  return rup128((size_t)T * fwd_rec_elems(nx, nu, elem, diag) * elem);
+}
 inline size_t fwd_workspace_bytes(int B, int T, int nx, int nu, int elem, bool diag) {
-  return 256 + fwd_gain_bytes(B, T, nx, nu, elem) + (size_t)B * T * fwd_rec_elems(nx, nu, elem, diag) * elem;
+  return 256 + (size_t)B * (fwd_gain_stride(T, nx, nu, elem) + fwd_rec_stride(T, nx, nu, elem, diag));
 }
 
 template <class M, int G, bool DIAG, class R>
@@ -116,9 +122,13 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
     if (cudaMallocAsync(&ws, wsb, s) != cudaSuccess) return fail("forward: workspace allocation of %zu bytes failed", wsb);
     own = true;
   }
+  const size_t gs = fwd_gain_stride(p->T, M::NX, M::NU, (int)sizeof(R));
+  const size_t ps = fwd_rec_stride(p->T, M::NX, M::NU, (int)sizeof(R), DIAG);
   a.ctr = (int*)ws;
   a.Kw = (unsigned char*)ws + 256;
-  a.Pw = (unsigned char*)ws + 256 + fwd_gain_bytes(p->B, p->T, M::NX, M::NU, (int)sizeof(R));
+  a.Pw = (unsigned char*)ws + 256 + (size_t)p->B * gs;
+  a.kw_stride = (long long)(gs / sizeof(R));
+  a.pw_stride = (long long)(ps / sizeof(R));
   cudaMemsetAsync(ws, 0, sizeof(int), s);
   kern<<<blocks, a.gpb * G, smem, s>>>(a);
   g_launches.fetch_add(1);

@@ -115,14 +115,15 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
   using D = Dims<M, DIAG, R>;
   const R* src = Cg + (size_t)t * D::NCS;
   R* dst = S.Cb(buf);
+  const uint64_t pol = l2_evict_first_policy();
   if constexpr (DIAG) {
-    for (int e = lane; e < D::NZ; e += G) cp_async_elem(dst + e, src + e);
+    for (int e = lane; e < D::NZ; e += G) cp_async_elem(dst + e, src + e, pol);
   } else {
     // element e -> padded (row, col); advanced incrementally (no div/mod per element)
     int col = lane % D::NZ, off = (lane / D::NZ) * D::ZLD + col;
 #pragma unroll 4
     for (int e = lane; e < D::NCS; e += G) {
-      cp_async_elem(dst + off, src + e);
+      cp_async_elem(dst + off, src + e, pol);
       col += G;
       off += G;
       if constexpr (G <= D::NZ) {  // at most one wrap: branch-free select
@@ -140,7 +141,7 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
   if (cg) {
     const R* s2 = cg + (size_t)t * D::NZ;
     R* d2 = S.cb(buf);
-    for (int e = lane; e < D::NZ; e += G) cp_async_elem(d2 + e, s2 + e);
+    for (int e = lane; e < D::NZ; e += G) cp_async_elem(d2 + e, s2 + e, pol);
   }
 }
 
