@@ -38,6 +38,9 @@ struct DoubleIntegrator {
   DMPC_DEV static void prep(const S*, S* P) { P[0] = S(0); }
   // structural nonzeros of A = df/dx and B = df/du (compile-time; zero terms are skipped)
   __host__ __device__ static constexpr bool a_nz(int r, int c) { return r == c || (r < D && c == r + D); }
+  // entries that are the constant 1 (A = I + dt df/dx: the diagonal) or exactly dt
+  __host__ __device__ static constexpr bool a_one(int r, int c) { return r == c; }
+  __host__ __device__ static constexpr bool a_dt(int r, int c) { return r < D && c == r + D; }
   __host__ __device__ static constexpr bool b_nz(int r, int c) { return r >= D && r - D == c; }
   template <class S>
   DMPC_DEV static void step(const S*, S dt, const S* x, const S* u, S* o) {
@@ -76,6 +79,8 @@ struct PlanarQuad {
     return r == c || (r < 3 && c == r + 3) || ((r == 3 || r == 4) && c == 2);
   }
   __host__ __device__ static constexpr bool b_nz(int r, int c) { return r >= 3 && c >= 0; }
+  __host__ __device__ static constexpr bool a_one(int r, int c) { return r == c; }
+  __host__ __device__ static constexpr bool a_dt(int r, int c) { return r < 3 && c == r + 3; }
   // P = [m, arm, I, g, 1/m, arm/I]
   template <class S>
   DMPC_DEV static void prep(const S* th, S* P) {
@@ -158,6 +163,8 @@ struct Quad13 {
            (r >= 10 && c >= 10);                                       // gyroscopic terms
   }
   __host__ __device__ static constexpr bool b_nz(int r, int c) { return r >= 7 && c >= 0; }
+  __host__ __device__ static constexpr bool a_one(int r, int c) { return r == c; }
+  __host__ __device__ static constexpr bool a_dt(int r, int c) { return r < 3 && c == r + 7; }
   // P = [m, arm, Jx, Jy, Jz, kappa, g, 1/m, arm/sqrt2, 1/Jx, 1/Jy, 1/Jz, Jz-Jy, Jx-Jz, Jy-Jx]
   template <class S>
   DMPC_DEV static void prep(const S* th, S* P) {
@@ -307,6 +314,8 @@ struct LinearModel {
   static constexpr int NX = NX_, NU = NU_, NTH = NX_ * NX_ + NX_ * NU_, NP = 1, KIND = 2;
   __host__ __device__ static constexpr bool a_nz(int, int) { return true; }  // dense
   __host__ __device__ static constexpr bool b_nz(int, int) { return true; }
+  __host__ __device__ static constexpr bool a_one(int, int) { return false; }
+  __host__ __device__ static constexpr bool a_dt(int, int) { return false; }
   static constexpr bool kLinearParams = true;
 };
 

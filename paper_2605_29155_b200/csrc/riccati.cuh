@@ -222,6 +222,20 @@ struct CostPipe {
 template <int G, int RPL>
 DMPC_DEV int row_of(int lane, int k) { return lane + k * G; }
 
+// Entry classes of A_t: structural zero, the constant 1 (diagonal of I + dt df/dx), exactly
+// dt (kinematic couplings), or state-dependent (read from the shared-memory copy). A row
+// with no state-dependent entry is never loaded.
+template <class M>
+__host__ __device__ constexpr bool a_sd(int r, int c) {
+  return M::a_nz(r, c) && !M::a_one(r, c) && !M::a_dt(r, c);
+}
+template <class M>
+__host__ __device__ constexpr bool a_row_sd(int r) {
+  bool any = false;
+  for (int c = 0; c < M::NX; c++) any = any || a_sd<M>(r, c);
+  return any;
+}
+
 template <class M>
 __host__ __device__ constexpr bool b_row_nz(int r) {
   bool any = false;
@@ -233,7 +247,7 @@ __host__ __device__ constexpr bool b_row_nz(int r) {
 // A_t / B_t (M::a_nz / M::b_nz, compile-time) are skipped; the row of A is the same for
 // every lane, so the skipping is uniform (no divergence).
 template <class M, bool DIAG, class R, int G, int RPL>
-DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][M::NX]) {
+DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][M::NX], R dt) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
   R ma[RPL][NX], nb[RPL][NU];
@@ -247,14 +261,17 @@ DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][
 #pragma unroll
   for (int r = 0; r < NX; r++) {
     R arow[NX], brow[NU];
-    lds_row<NX>(S.As + r * D::LDA, arow);
+    if (a_row_sd<M>(r)) lds_row<NX>(S.As + r * D::LDA, arow);
     if (b_row_nz<M>(r)) lds_row<NU>(S.Bs + r * D::LDB, brow);
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
       const R v = vxx[k][r];
 #pragma unroll
-      for (int b = 0; b < NX; b++)
-        if (M::a_nz(r, b)) ma[k][b] += v * arow[b];
+      for (int b = 0; b < NX; b++) {
+        if (M::a_one(r, b)) ma[k][b] += v;
+        else if (M::a_dt(r, b)) ma[k][b] += v * dt;
+        else if (M::a_nz(r, b)) ma[k][b] += v * arow[b];
+      }
 #pragma unroll
       for (int b = 0; b < NU; b++)
         if (M::b_nz(r, b)) nb[k][b] += v * brow[b];
@@ -278,7 +295,7 @@ DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][
 // operand is again a row of A, so its structural zeros are skipped without divergence.
 template <class M, bool DIAG, class R, int G, int RPL>
 DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&qxx)[RPL][M::NX],
-                          R (&quxc)[RPL][M::NU]) {
+                          R (&quxc)[RPL][M::NU], R dt) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
   int ac[RPL];  // clamped row index (padding rows alias the last row; never stored)
@@ -301,14 +318,17 @@ DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&q
 #pragma unroll
   for (int r = 0; r < NX; r++) {
     R arow[NX], brow[NU];
-    lds_row<NX>(S.As + r * D::LDA, arow);
+    if (a_row_sd<M>(r)) lds_row<NX>(S.As + r * D::LDA, arow);
     if (b_row_nz<M>(r)) lds_row<NU>(S.Bs + r * D::LDB, brow);
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
       const R mra = S.MA[r * D::LDA + ac[k]];
 #pragma unroll
-      for (int bb = 0; bb < NX; bb++)
-        if (M::a_nz(r, bb)) qxx[k][bb] += mra * arow[bb];
+      for (int bb = 0; bb < NX; bb++) {
+        if (M::a_one(r, bb)) qxx[k][bb] += mra;
+        else if (M::a_dt(r, bb)) qxx[k][bb] += mra * dt;
+        else if (M::a_nz(r, bb)) qxx[k][bb] += mra * arow[bb];
+      }
 #pragma unroll
       for (int i = 0; i < NU; i++)
         if (M::b_nz(r, i)) quxc[k][i] += brow[i] * mra;
