@@ -32,7 +32,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--minibatch", type=int, default=2048, help="samples per rank per step")
     ap.add_argument("--T", type=int, default=10)
+    ap.add_argument("--mode", default="update", choices=["update", "train"],
+                    help="update: PPO minibatch steps (13-state quadrotor); train: full device-resident "
+                         "PPO iterations (batched race env rollout collection + update, planar model)")
+    ap.add_argument("--envs", type=int, default=1024, help="train mode: environments per GPU")
+    ap.add_argument("--rollout-steps", type=int, default=32, help="train mode: steps per update")
     args = ap.parse_args()
+    if args.mode == "train":
+        return train_mode(args)
 
     import torch
     import torch.distributed as dist
@@ -101,6 +108,79 @@ def main():
                        "allreduce_bytes": reducer.nbytes, "parallelism": f"dp{world}"},
             "diffmpc_launches_per_step": launches,
             "mean_solver_iters": float(sink.get("iterations", 0)) / max(1, sink.get("solves", 1)),
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def train_mode(args):
+    """Full PPO iterations on the device: collect (envs x rollout-steps) transitions with
+    one batched DiffMPC forward per step on the GPU race environments, GAE, then one epoch
+    of minibatch updates (DiffMPC forward + backward per minibatch, one NCCL all-reduce)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_29155_b200 import DynModel, SolveSettings, _lib, ppo, raceenv
+    from paper_2605_29155_b200.layer import MpcSolver
+    from paper_2605_29155_b200.policy import CostHeadScaling, PolicyBundle
+    from paper_2605_29155_b200.rollout import DeviceRollout
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    model = DynModel.planar_quadrotor(dt=0.05)
+    st = SolveSettings(T=args.T, u_min=0.0, u_max=2 * 0.5 * 9.81)
+    torch.manual_seed(0)
+    bundle = PolicyBundle("ac_mpc", raceenv.OBS_DIM, model, st, CostHeadScaling.for_model(model, 6)).to(dev)
+    env = raceenv.BatchedRaceEnv(raceenv.hairpin5(), model, args.envs, device=dev, seed=11 + rank)
+    solver = MpcSolver(model, st, device=dev)
+    cfg = ppo.TrainConfig(steps_per_update=args.rollout_steps, minibatch_size=args.minibatch, sgd_epochs=1)
+    opt = torch.optim.Adam(bundle.parameters(), lr=cfg.lr_start)
+    reducer = ppo.GradAllReduce(bundle.parameters())
+    col = DeviceRollout(bundle, solver, env, cfg, seed=5 + rank)
+    gen = torch.Generator().manual_seed(3)
+
+    def iteration():
+        flat, stats = col.collect()
+        m = ppo.ppo_update(flat, bundle, opt, cfg, solver, generator=gen, reducer=reducer, rank=rank, world=world)
+        return stats, m
+
+    for _ in range(max(1, args.warmup // 3)):
+        iteration()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = _lib.launch_count()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K = max(2, args.steps // 10)
+    a.record()
+    for _ in range(K):
+        stats, m = iteration()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / K
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        samples = args.envs * args.rollout_steps
+        print(json.dumps({
+            "metric": "AC-MPC PPO iterations/s (device-resident rollout + update, planar race env)",
+            "value": 1e3 / ms, "unit": "iterations/s", "env_steps_per_s": world * samples * 1e3 / ms,
+            "n_gpus": world, "iterations": K, "ms_per_iteration": ms, "higher_is_better": True,
+            "scaling": "weak", "dtype": "f32", "data": "synthetic (race env, random-init policy)",
+            "config": {"workload": "PPO: collect envs x steps with one DiffMPC forward per step, GAE, "
+                                   "1 epoch of minibatch updates", "T": args.T, "envs_per_gpu": args.envs,
+                       "rollout_steps": args.rollout_steps, "minibatch_per_gpu": args.minibatch // world,
+                       "parallelism": f"dp{world}"},
+            "diffmpc_launches_per_iteration": (_lib.launch_count() - l0) / K,
+            "mean_solver_iters": float(stats["solver_iters"]) / stats["solves"],
+            "episodes_last_iteration": int(stats["episodes"]),
         }), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -222,6 +222,14 @@ def backward_raw(model, settings, C, c, X, U, dLdX=None, dLdU=None, dLdJ=None, *
 
 def dynamics(model, x, u, *, dtype=torch.float64, device=None, want_jac=True, theta=None):
     """Batched f(x,u) and Jacobians on the GPU; returns numpy arrays (N,nx), (N,nx,nx), (N,nx,nu)."""
+    cpu = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
+    return tuple(cpu(t) for t in dynamics_t(model, x, u, dtype=dtype, device=device, want_jac=want_jac,
+                                           theta=theta))
+
+
+def dynamics_t(model, x, u, *, dtype=torch.float64, device=None, want_jac=False, theta=None):
+    """Device-resident variant of ``dynamics``: returns torch tensors (xn, A, Bm) on the device,
+    enqueued on the current stream (used by the batched environment step)."""
     dev = _device(device)
     nx, nu = model.n_x, model.n_u
     x = _as(x, dtype, dev, name="x")
@@ -239,5 +247,4 @@ def dynamics(model, x, u, *, dtype=torch.float64, device=None, want_jac=True, th
     P = _abi.ptr
     with torch.cuda.device(dev):
         _lib.check(fn(ctypes.byref(p), N, P(th), P(x), P(u), P(xn), P(A), P(Bm), _stream()))
-    cpu = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
-    return cpu(xn), cpu(A), cpu(Bm)
+    return xn, A, Bm

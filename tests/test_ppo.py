@@ -146,3 +146,36 @@ def test_ac_mpc_minibatch_step_on_gpu():
     assert loss is not None and torch.isfinite(loss)
     moved = sum(float((p.detach() - q).abs().sum()) for p, q in zip(b.actor.parameters(), before))
     assert moved > 0.0  # the cost actor is trained through the DiffMPC layer
+
+
+@pytest.mark.gpu
+def test_device_rollout_collect_and_update():
+    """§8(f) row 2: device-resident collection on the batched race env, then a PPO update
+    whose first minibatch re-solve reproduces the rollout controls (ratio 1)."""
+    from paper_2605_29155_b200 import raceenv
+    from paper_2605_29155_b200.layer import MpcSolver
+    from paper_2605_29155_b200.rollout import DeviceRollout
+
+    dev = torch.device("cuda")
+    model = DynModel.planar_quadrotor(dt=0.05)
+    st = SolveSettings(T=5, u_min=0.0, u_max=2 * 0.5 * 9.81)
+    torch.manual_seed(0)
+    b = PolicyBundle("ac_mpc", raceenv.OBS_DIM, model, st, CostHeadScaling.for_model(model, 6),
+                     hidden=(64, 64)).to(dev)
+    env = raceenv.BatchedRaceEnv(raceenv.hairpin5(), model, 128, device=dev, seed=1)
+    solver = MpcSolver(model, st, device=dev)
+    cfg = ppo.TrainConfig(steps_per_update=6, minibatch_size=256, sgd_epochs=1)
+    col = DeviceRollout(b, solver, env, cfg, seed=2)
+    flat, stats = col.collect()
+    assert flat["obs"].shape == (6 * 128, raceenv.OBS_DIM) and flat["U_warm"].shape == (6 * 128, 5, 2)
+    for k, v in flat.items():
+        assert bool(torch.isfinite(v).all()), k
+    batch = {"obs": flat["obs"][:256], "actions": flat["actions"][:256], "old_log_probs": flat["log_probs"][:256],
+             "advantages": flat["advantages"][:256].float(), "returns": flat["returns"][:256].float(),
+             "x_init": flat["x_init"][:256], "U_warm": flat["U_warm"][:256]}
+    _, metrics = ppo.ppo_losses(b, batch, cfg, solver)
+    assert abs(float(metrics["mean_ratio"]) - 1.0) < 1e-5
+    opt = torch.optim.Adam(b.parameters(), lr=1e-4)
+    out = ppo.ppo_update(flat, b, opt, cfg, solver, generator=torch.Generator().manual_seed(0))
+    assert out["skipped_minibatches"] == 0
+    assert int(stats["solves"]) == 6 * 128
