@@ -128,20 +128,23 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     for (int e = lane; e < (T + 1) * NX; e += G) {
       const int t = e / NX, i = e % NX;
       Xs[t * LDA + i] = xg[e];
-      dXs[t * LDA + i] = R(0);
+      // the seeds dL/dX, dL/dU are parked in dX / dU (free until the differential
+      // rollout) so the sweep reads them from shared memory, not global
+      dXs[t * LDA + i] = sXg ? sXg[e] : R(0);
     }
     const R* ug = (const R*)args.U + (size_t)pid * T * NU;
     for (int e = lane; e < T * NU; e += G) {
       const R v = ug[e];
       const int t = e / NU, r = e % NU;
       Us[t * LDB + r] = v;
-      dUs[t * LDB + r] = R(0);
+      dUs[t * LDB + r] = sUg ? sUg[e] : R(0);
       // clamped = (U <= u_min) | (U >= u_max)  (policy.py:271)
       cl[e] = (uint8_t)((double)v <= args.u_min[r] || (double)v >= args.u_max[r]);
     }
   }
   // V_x = dL/dX_T, V_xx = 0 (gradlayer.py:106-107)
-  for (int e = lane; e < NX; e += G) S.Vx[e] = sXg ? sXg[T * NX + e] : R(0);
+  __syncwarp(gm);
+  for (int e = lane; e < NX; e += G) S.Vx[e] = dXs[T * LDA + e];
   __syncwarp(gm);
 
   // ======================= auxiliary Riccati sweep (kernels.py:582-707) =========
@@ -168,13 +171,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
 #pragma unroll
       for (int k = 0; k < RPL; k++) {
         const int a = min(row_of<G, RPL>(lane, k), NX - 1);
-        R s = sXg ? sXg[t * NX + a] : R(0);
+        R s = dXs[t * LDA + a];
 #pragma unroll
         for (int b2 = 0; b2 < NX; b2++) s += S.As[b2 * LDA + a] * vx[b2];
         qx[k] = s;
       }
       for (int a = lane; a < NU; a += G) {
-        R s = sUg ? sUg[t * NU + a] : R(0);
+        R s = dUs[t * LDB + a];
 #pragma unroll
         for (int b2 = 0; b2 < NX; b2++) s += S.Bs[b2 * LDB + a] * vx[b2];
         S.qu[a] = s;
@@ -274,8 +277,15 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       for (int e = lane; e < NX; e += G) ((R*)args.dx0)[(size_t)pid * NX + e] = R(0);
     if (want_theta)
       for (int e = lane; e < args.n_theta; e += G) ((R*)args.dtheta)[(size_t)pid * args.n_theta + e] = R(0);
+    __syncwarp(gm);
+    for (int e = lane; e < (T + 1) * LDA; e += G) dXs[e] = R(0);  // (held the seeds)
+    for (int e = lane; e < T * LDB; e += G) dUs[e] = R(0);
+    __syncwarp(gm);
   } else {
     // ============ differential rollout + assembly (kernels.py:710-756) ============
+    __syncwarp(gm);
+    for (int e = lane; e < NX; e += G) dXs[e] = R(0);  // dX_0 = 0 (seeds no longer needed)
+    __syncwarp(gm);
     for (int t = 0; t < T; t++) {
       R xr[NX], ur[NU];
       lds_row<NX>(Xs + t * LDA, xr);
