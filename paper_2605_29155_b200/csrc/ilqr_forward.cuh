@@ -66,6 +66,7 @@ struct FwdArgs {
   long long kw_stride, pw_stride;  // per-problem workspace strides (elements of R, 128-byte multiples)
   int* ctr;            // per-launch work counter (zeroed before the launch)
   int pw;              // problems per warp claimed by one atomicAdd (32/G, or gpb if smaller)
+  int claim_group;     // 1: each group claims its own problems (DIFFMPC_CLAIM=group)
 };
 
 __host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a * a; }
@@ -159,16 +160,24 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   R* Kb = (R*)(base + L.oKb);
   Ric<M, DIAG, R> S;
   S.bind(base, L.ric);
-  const int units = (args.B + pw - 1) / pw;
+  // per_group: every group claims its own next problem (the groups of a warp then run
+  // independent instruction streams); otherwise the warp's groups claim together
+  const bool per_group = args.claim_group != 0;
+  const int upw = per_group ? 1 : pw;
+  const int units = (args.B + upw - 1) / upw;
 
   auto claim = [&]() -> int {
     int u = 0;
+    if (per_group) {
+      if (lane == 0) u = atomicAdd(args.ctr, 1);
+      return __shfl_sync(gm, u, 0, G);
+    }
     if ((threadIdx.x & 31) == 0) u = atomicAdd(args.ctr, 1);
     return __shfl_sync(wmask, u, 0);
   };
 
   for (int unit = claim(); unit < units; unit = claim()) {
-  const int pid = unit * pw + gi;
+  const int pid = per_group ? unit : unit * pw + gi;
   if (pid < args.B) {
   double* Un = Ubuf0;  // nominal controls (swapped with the alpha_0 candidate's on accept)
   double* Us = Ubuf1;

@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -108,6 +109,14 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
     a.gpb = g;
   }
   a.pw = (32 / G < a.gpb) ? 32 / G : a.gpb;
+  {
+    static int cg = -1;
+    if (cg < 0) {
+      const char* e = getenv("DIFFMPC_CLAIM");
+      cg = (e && std::string(e) == "group") ? 1 : 0;
+    }
+    a.claim_group = cg;
+  }
   const int smem = a.gpb * a.smem_stride;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   // persistent grid: at most the resident blocks; warps claim problems dynamically
