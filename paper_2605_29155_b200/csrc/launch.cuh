@@ -10,6 +10,7 @@
 
 #include "../../include/diffmpc.h"
 #include "ilqr_backward.cuh"
+#include "ilqr_forward_lat.cuh"
 
 namespace dmpc {
 
@@ -100,6 +101,28 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   a.X = io->X; a.U = io->U; a.J = io->J; a.K = io->K; a.k = io->k; a.iters = io->iters;
   a.converged = io->converged; a.diverged = io->diverged; a.fail_t = io->fail_t;
   a.clamped = io->clamped; a.alpha_hist = io->alpha_hist; a.J_hist = io->J_hist;
+  // Small batches take the latency-oriented kernel (one block per problem) while the
+  // grid cannot fill the GPU with the throughput mapping; DIFFMPC_FWD=lat|tput forces one.
+  {
+    static int mode = -1, lat_max = 0;
+    if (mode < 0) {
+      const char* e = getenv("DIFFMPC_FWD");
+      mode = (e && std::string(e) == "lat") ? 1 : ((e && std::string(e) == "tput") ? 2 : 0);
+      const char* m = getenv("DIFFMPC_LAT_MAX");
+      lat_max = m ? atoi(m) : 2 * num_sms();
+    }
+    const LatLayout<M, DIAG, R> LL = LatLayout<M, DIAG, R>::make(p->T, p->n_alpha);
+    const bool fits = LL.total <= max_smem_optin() - 1024;
+    if (fits && (mode == 1 || (mode == 0 && p->B <= lat_max))) {
+      auto lk = ilqr_forward_lat_kernel<M, DIAG, R>;
+      if (LL.total > 48 * 1024) cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, LL.total);
+      lk<<<p->B, kLatThreads, LL.total, s>>>(a);
+      g_launches.fetch_add(1);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return fail("forward (latency) launch failed: %s", cudaGetErrorString(e));
+      return 0;
+    }
+  }
   auto kern = ilqr_forward_kernel<M, G, DIAG, R>;
   int per_sm = 1;
   if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)) return -1;

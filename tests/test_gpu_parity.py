@@ -126,3 +126,37 @@ def test_dynamics_vs_reference():
         np.testing.assert_allclose(xn, d[f"{name}_xn"], rtol=1e-13, atol=1e-13)
         np.testing.assert_allclose(A, d[f"{name}_A"], rtol=1e-13, atol=1e-13)
         np.testing.assert_allclose(B, d[f"{name}_B"], rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.gpu
+def test_latency_kernel_matches_throughput_kernel():
+    """The small-batch (block-per-problem) forward and the throughput forward solve the same
+    problems to the same iterates: identical iteration counts / masks, f32 round-off apart."""
+    import subprocess
+    import sys
+
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2605_29155_b200 import DynModel, problems, solver
+m = DynModel.quadrotor()
+pb = problems.random_problem(m, 96, 10, seed=21)
+o = solver.solve_raw(m, pb.settings, pb.x0, pb.dense_C(), pb.c, pb.U_warm)
+np.savez(sys.argv[1], U=o.U.cpu().numpy(), X=o.X.cpu().numpy(), it=o.iters.cpu().numpy(),
+         cl=o.clamped.cpu().numpy(), J=o.J.cpu().numpy())
+'''
+    import os
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("lat", "tput"):
+        f = os.path.join(tempfile.mkdtemp(), f"{mode}.npz")
+        env = dict(os.environ, DIFFMPC_FWD=mode)
+        subprocess.run([sys.executable, "-c", code, f], check=True, cwd=root, env=env)
+        outs[mode] = np.load(f)
+    a, b = outs["lat"], outs["tput"]
+    np.testing.assert_array_equal(a["it"], b["it"])
+    np.testing.assert_array_equal(a["cl"], b["cl"])
+    np.testing.assert_allclose(a["U"], b["U"], rtol=1e-4, atol=1e-4)
+    np.testing.assert_allclose(a["J"], b["J"], rtol=1e-5)

@@ -158,3 +158,26 @@ def test_dynamics_quad13_vs_oracle():
     np.testing.assert_allclose(xn, rxn, rtol=1e-14, atol=1e-14)
     np.testing.assert_allclose(A, rA, rtol=1e-13, atol=1e-13)
     np.testing.assert_allclose(B, rB, rtol=1e-13, atol=1e-13)
+
+
+def test_latency_kernel_repeatable_across_waves():
+    """The block-per-problem forward gives bit-identical results across repeated launches,
+    including blocks of a second wave that inherit another block's shared memory (guards
+    the block-wide initialisation ordering)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, torch
+sys.path.insert(0, ".")
+from paper_2605_29155_b200 import DynModel, problems, solver
+pb = problems.random_problem(DynModel.quadrotor(), 300, 10, seed=1)
+C = pb.dense_C()
+ref = solver.solve_raw(pb.model, pb.settings, pb.x0, C, pb.c, pb.U_warm)
+for i in range(30):
+    a = solver.solve_raw(pb.model, pb.settings, pb.x0, C, pb.c, pb.U_warm)
+    assert torch.equal(a.X, ref.X) and torch.equal(a.K, ref.K) and torch.equal(a.iters, ref.iters), i
+'''
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=dict(os.environ, DIFFMPC_FWD="lat"))
