@@ -217,6 +217,32 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
     return part;
   };
 
+  // lane i < NZ's share z_i (0.5 (C_t z)_i + c_i) of the stage cost, branch-free (lanes >= NZ
+  // read row NZ-1 and contribute 0) so the scheduler can overlap it with the dynamics; the
+  // line search sums these shares per lane over the horizon and reduces once at the end.
+  auto lane_cost = [&](const R* C_t, const R* c_t, const double (&x)[NX], const double (&u)[NU]) -> double {
+    double z[NZ];
+#pragma unroll
+    for (int i = 0; i < NX; i++) z[i] = x[i];
+#pragma unroll
+    for (int i = 0; i < NU; i++) z[NX + i] = u[i];
+    const int row = lane < NZ ? lane : NZ - 1;
+    double zi = 0.0;
+#pragma unroll
+    for (int k = 0; k < NZ; k++)
+      if (lane == k) zi = z[k];
+    if constexpr (DIAG) {
+      return 0.5 * zi * ((double)C_t[row] * zi) + (double)c_t[row] * zi;
+    } else {
+      R crow[NZ];
+      lds_row<NZ>(C_t + row * ZLD, crow);
+      double ra[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < NZ; j++) ra[j & 3] += (double)crow[j] * z[j];
+      return 0.5 * zi * ((ra[0] + ra[1]) + (ra[2] + ra[3])) + (double)c_t[row] * zi;
+    }
+  };
+
   // =========================== initial rollout (kernels.py:161-178), warp 0 =========
   if (warp == 0) {
     double x[NX];
@@ -493,32 +519,31 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
       double* Uc = Ubuf(cb);
       double x[NX];
       lds_row_d<NX>(Xn, x);
-      double Jm = 0.0;
+      double Jl = 0.0;  // this lane's share of the candidate cost, summed over t
       bool dm = false;
       for (int t = 0; t < T; t++) {
+        // nominal row, controls, gains: independent of the candidate state
         double xbar[NX];
         lds_row_d<NX>(Xn + t * XLD, xbar);
-        double v = 0.0;
-        if (lane < NU) {
-          v = Un[t * ULD + lane] + alpha * kg[t * ULD + lane];
-          R krow[NX];
-          lds_row<NX>(Ks + (t * NU + lane) * LDA, krow);
-          v = feedback<NX>(v, krow, x, xbar);
-          const double lo = args.u_min[lane], hi = args.u_max[lane];
-          if (v < lo) v = lo;
-          else if (v > hi) v = hi;
-          Uc[t * ULD + lane] = v;
-        }
+        const int r = lane < NU ? lane : 0;
+        double v = Un[t * ULD + r] + alpha * kg[t * ULD + r];
+        R krow[NX];
+        lds_row<NX>(Ks + (t * NU + r) * LDA, krow);
+        v = feedback<NX>(v, krow, x, xbar);
+        const double lo = args.u_min[r], hi = args.u_max[r];
+        if (v < lo) v = lo;
+        else if (v > hi) v = hi;
         double u[NU];
 #pragma unroll
-        for (int r = 0; r < NU; r++) u[r] = __shfl_sync(0xffffffffu, v, r);
+        for (int q = 0; q < NU; q++) u[q] = __shfl_sync(0xffffffffu, v, q);
+        double xn[NX];
+        step_e<M, R>(P_e, dt_e, As, LDA, Bs, LDB, x, u, xn);  // critical path first
+        Jl += lane_cost(Cs + t * NCSP, cs + t * ZLD, x, u);   // overlaps the dynamics
+        if (lane < NU) Uc[t * ULD + lane] = v;
 #pragma unroll
         for (int i = 0; i < NX; i++)
           if (lane == i) Xc[t * XLD + i] = x[i];
-        Jm += warp_cost(Cs + t * NCSP, cs + t * ZLD, x, u);
-        double xn[NX];
-        step_e<M, R>(P_e, dt_e, As, LDA, Bs, LDB, x, u, xn);
-        bool fin = finite_(Jm);
+        bool fin = true;
 #pragma unroll
         for (int i = 0; i < NX; i++) {
           fin &= finite_(xn[i]);
@@ -529,6 +554,12 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
 #pragma unroll
       for (int i = 0; i < NX; i++)
         if (lane == i) Xc[T * XLD + i] = x[i];
+      // one reduction per candidate; a non-finite stage cost leaves a non-finite sum (dead)
+      if (lane >= NZ) Jl = 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) Jl += __shfl_xor_sync(0xffffffffu, Jl, off);
+      const double Jm = Jl;
+      dm |= !finite_(Jm);
       if (lane == 0) {
         Jc[a] = dm ? INFINITY : Jm;
         deadc[a] = dm;
