@@ -247,8 +247,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   __syncwarp(gm);
 
   // stage cost 0.5 z'Cz + c'z in double (_stage_cost_xu, kernels.py:133-145); rows of the
-  // dense quadratic form are split over the LCX lanes of a slot (j = lane in slot) and
-  // reduced with xor shuffles (every lane ends with the identical sum).
+  // dense quadratic form are split over the LCX lanes of a slot (j = lane in slot). Each
+  // lane returns its share; callers sum the shares over the horizon and reduce once
+  // (sum_lanes, below) — no shuffle chain per stage. Diagonal costs are computed whole by
+  // every lane.
   auto stage_cost = [&](auto lcx_tag, const R* Cs, const R* cs, const double* x, const double* u,
                         int j, unsigned smask) -> double {
     constexpr int LCX = decltype(lcx_tag)::value;
@@ -284,10 +286,16 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           part += 0.5 * zi * row + (double)cs[i] * zi;
         }
       }
-#pragma unroll
-      for (int off = LCX / 2; off > 0; off >>= 1) part += __shfl_xor_sync(smask, part, off, G);
       return part;
     }
+  };
+  auto sum_lanes = [&](auto lcx_tag, double part, unsigned smask) -> double {
+    constexpr int LCX = decltype(lcx_tag)::value;
+    if constexpr (!DIAG) {
+#pragma unroll
+      for (int off = LCX / 2; off > 0; off >>= 1) part += __shfl_xor_sync(smask, part, off, G);
+    }
+    return part;
   };
 
   double J = 0.0;
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       fwdp.pack_out(Pw, t);
       double u[NU];
       lds_row_d<NU>(Un + t * ULD, u);
-      J += stage_cost(std::integral_constant<int, G>{}, fwdp.C(t), fwdp.c(t), xc, u, lane, gm);
+      J += stage_cost(std::integral_constant<int, G>{}, fwdp.C(t), fwdp.c(t), xc, u, lane, gm);  // lane share
       __syncwarp(gm);
       fwdp.release(t);
       double xn[NX];
@@ -327,11 +335,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       if (!fin) {
         fail_t = t;
         active = 0;
-        J = INFINITY;
         diverged = 1;  // rollout_failed (ilqr.py:196-200)
         break;
       }
     }
+    J = sum_lanes(std::integral_constant<int, G>{}, J, gm);
+    if (fail_t >= 0) J = INFINITY;
     cp_async_wait_all();
     __syncwarp(gm);
   }
@@ -540,7 +549,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           lsp.release(t);
           double xn[NX];
           step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
-          bool fin = finite_(Jm);
+          bool fin = true;
 #pragma unroll
           for (int i = 0; i < NX; i++) {
             fin &= finite_(xn[i]);
@@ -555,6 +564,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
             if ((i % LC) == j) Xn[T * XLD + i] = xc[i];
         }
         cp_async_wait_all();
+        // one reduction per candidate; a non-finite stage cost leaves a non-finite sum
+        Jm = sum_lanes(std::integral_constant<int, LC>{}, Jm, smask);
+        dm |= !finite_(Jm);
         if (dm) Jm = INFINITY;
 #pragma unroll
         for (int s = 0; s < NSLOT; s++) {
