@@ -100,9 +100,14 @@ def main():
     sys.path.insert(0, ROOT)
     from bench import fp32_peak
     peak, _ = fp32_peak(dev)
+    # CPU samples first (a 3 s host phase would let the GPU clocks drop between cases),
+    # then warm the GPU (clocks, module load, allocator) before the first timed case
+    cpus = {T: (None if args.no_cpu else cpu_rate(model, T)) for T in args.T}
+    for _ in range(3):
+        time_case(model, 16384, 10, args.layout, dev, budget_s=0.3)
     rows = []
     for T in args.T:
-        cpu = None if args.no_cpu else cpu_rate(model, T)
+        cpu = cpus[T]
         for B in args.B:
             r = time_case(model, B, T, args.layout, dev)
             r["roofline_frac"] = r["fwd_tflops"] / peak
