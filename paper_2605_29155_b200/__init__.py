@@ -5,6 +5,10 @@ Public API (mirrors the reference package ``fusedmpc``):
     solve_raw / solve_diag / backward_raw               — array-level batch API (GPU)
     MpcSolver, MpcSolveLayer, mpc_control               — AC-MPC drop-in layer
     MPC, QuadCost                                       — mpc.pytorch-style module
+    policy, ppo, rollout, raceenv                       — AC-MPC training plumbing (PPO with
+                                                          one NCCL all-reduce, device-resident
+                                                          rollouts, batched GPU race env)
+    benchgrid                                           — latency grid in the bench CSV schema
 Heavy modules (torch, the CUDA library) are imported lazily.
 """
 

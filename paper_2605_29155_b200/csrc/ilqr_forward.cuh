@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   // every lane.
   auto stage_cost = [&](auto lcx_tag, const R* Cs, const R* cs, const double* x, const double* u,
                         int j, unsigned smask) -> double {
-    constexpr int LCX = decltype(lcx_tag)::value;
+    [[maybe_unused]] constexpr int LCX = decltype(lcx_tag)::value;
     double z[NZ];
 #pragma unroll
     for (int i = 0; i < NX; i++) z[i] = x[i];

@@ -119,3 +119,25 @@ def test_null_required_pointer_rejected():
     p = _problem()
     rc = L.diffmpc_forward_f32(ctypes.byref(p), ctypes.byref(_abi.DiffMPCForwardIO()), None)
     assert rc < 0 and "NULL" in L.diffmpc_last_error().decode()
+
+
+def test_forward_workspace_bytes_matches_layout():
+    """diffmpc_forward_workspace_bytes: 256-byte counter block + per-problem 128-byte aligned
+    gain rows (T x n_u x LDA) and stage records ([C_t padded | c_t padded])."""
+    import ctypes
+
+    from paper_2605_29155_b200 import DynModel, SolveSettings
+
+    L = _lib.lib()
+    m = DynModel.quadrotor()
+    st = SolveSettings(T=10, u_min=0.0, u_max=5.886)
+    rup = lambda v, a: (v + a - 1) // a * a  # noqa: E731
+    for layout, B in ((_abi.COST_DENSE, 3), (_abi.COST_DIAG, 5)):
+        p = _abi.make_problem(m, st, B, layout)
+        for elem in (4, 8):
+            vn = 16 // elem
+            lda, zld = rup(13, vn), rup(17, vn)
+            rec = (zld if layout == _abi.COST_DIAG else 17 * zld) + zld
+            want = 256 + B * (rup(10 * 4 * lda * elem, 128) + rup(10 * rec * elem, 128))
+            assert L.diffmpc_forward_workspace_bytes(ctypes.byref(p), elem) == want
+    assert L.diffmpc_forward_workspace_bytes(ctypes.byref(p), 3) == 0
