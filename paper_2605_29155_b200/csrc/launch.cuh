@@ -126,6 +126,16 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   auto kern = ilqr_forward_kernel<M, G, DIAG, R>;
   int per_sm = 1;
   if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)) return -1;
+  if (const char* e = getenv("DIFFMPC_GPB")) {  // tuning override (even, keeps warps full)
+    const int g = atoi(e);
+    if (g >= 2 && g % 2 == 0 && g * G <= 1024 && g * a.smem_stride <= max_smem_optin()) {
+      a.gpb = g;
+      const int smem_g = g * a.smem_stride;
+      if (smem_g > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g);
+      int nb = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, g * G, smem_g) == cudaSuccess && nb > 0) per_sm = nb;
+    }
+  }
   if (p->B < a.gpb) {  // small batch: one block of the next power of two >= B groups
     int g = 1;
     while (g < p->B) g *= 2;
