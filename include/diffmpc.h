@@ -61,6 +61,10 @@ extern "C" {
 #define DIFFMPC_COST_DENSE 0
 #define DIFFMPC_COST_DIAG  1
 
+#define DIFFMPC_KERNEL_AUTO       0
+#define DIFFMPC_KERNEL_THROUGHPUT 1
+#define DIFFMPC_KERNEL_LATENCY    2
+
 #define DIFFMPC_MAX_NU     8
 #define DIFFMPC_MAX_ALPHA  8
 
@@ -77,7 +81,11 @@ typedef struct DiffMPCProblem {
   int32_t boxqp_max_iter;  /* projected-Newton iterations per stage QP (ilqr.py:40)    */
   int32_t n_theta;         /* number of model parameters in theta                      */
   int32_t theta_stride;    /* 0: theta shared by the batch; n_theta: per problem        */
-  int32_t reserved0;
+  int32_t kernel_select;   /* forward mapping: 0 auto (block-per-problem latency kernel for
+                              B <= 2 x #SMs, persistent throughput kernel above), 1 always
+                              throughput, 2 always latency. Both solve the same algorithm;
+                              pin one when results must be bit-identical across batch sizes
+                              (e.g. PPO rollout vs minibatch re-solve, trainer.py:9-12)   */
   double dt;               /* model timestep                                           */
   double conv_tol;         /* relative cost-decrease tolerance (ilqr.py:39)            */
   double boxqp_tol;        /* projected-gradient tolerance (ilqr.py:41)                */

@@ -13,6 +13,16 @@ MAX_NU = 8
 MAX_ALPHA = 8
 COST_DENSE = 0
 COST_DIAG = 1
+KERNEL_AUTO, KERNEL_THROUGHPUT, KERNEL_LATENCY = 0, 1, 2
+_KERNELS = {"auto": KERNEL_AUTO, "throughput": KERNEL_THROUGHPUT, "latency": KERNEL_LATENCY}
+
+
+def kernel_code(kernel) -> int:
+    if isinstance(kernel, int) and kernel in _KERNELS.values():
+        return kernel
+    if kernel not in _KERNELS:
+        raise ConfigError(f"kernel must be one of {tuple(_KERNELS)}, got {kernel!r}")
+    return _KERNELS[kernel]
 ABI_VERSION = 2
 
 
@@ -29,7 +39,7 @@ class DiffMPCProblem(ctypes.Structure):
         ("boxqp_max_iter", ctypes.c_int32),
         ("n_theta", ctypes.c_int32),
         ("theta_stride", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("kernel_select", ctypes.c_int32),
         ("dt", ctypes.c_double),
         ("conv_tol", ctypes.c_double),
         ("boxqp_tol", ctypes.c_double),
@@ -55,7 +65,7 @@ class DiffMPCBackwardIO(ctypes.Structure):
         "dX", "dU", "fail_t")]
 
 
-def make_problem(model, settings, B: int, layout: int, theta_stride: int = 0) -> DiffMPCProblem:
+def make_problem(model, settings, B: int, layout: int, theta_stride: int = 0, kernel="auto") -> DiffMPCProblem:
     """Fill a DiffMPCProblem from the reference-style model/settings objects."""
     nu = model.n_u
     if nu > MAX_NU:
@@ -75,6 +85,7 @@ def make_problem(model, settings, B: int, layout: int, theta_stride: int = 0) ->
     p.boxqp_max_iter = int(settings.boxqp_max_iter)
     p.n_theta = int(model.params.shape[0])
     p.theta_stride = int(theta_stride)
+    p.kernel_select = kernel_code(kernel)
     p.dt = float(model.dt)
     p.conv_tol = float(settings.conv_tol)
     p.boxqp_tol = float(settings.boxqp_tol)

@@ -96,6 +96,8 @@ int check_problem(const DiffMPCProblem* p) {
     return fail("unknown cost layout %d", p->cost_layout);
   if (p->theta_stride != 0 && p->theta_stride != p->n_theta)
     return fail("theta_stride must be 0 or n_theta");
+  if (p->kernel_select < DIFFMPC_KERNEL_AUTO || p->kernel_select > DIFFMPC_KERNEL_LATENCY)
+    return fail("unknown kernel_select %d", p->kernel_select);
   return 0;
 }
 

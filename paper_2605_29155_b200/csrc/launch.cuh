@@ -113,7 +113,9 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
     }
     const LatLayout<M, DIAG, R> LL = LatLayout<M, DIAG, R>::make(p->T, p->n_alpha);
     const bool fits = LL.total <= max_smem_optin() - 1024;
-    if (fits && (mode == 1 || (mode == 0 && p->B <= lat_max))) {
+    // per-call choice (kernel_select) wins; DIFFMPC_FWD only steers the auto choice
+    const int sel = p->kernel_select != DIFFMPC_KERNEL_AUTO ? p->kernel_select : (mode == 1 ? 2 : (mode == 2 ? 1 : 0));
+    if (fits && (sel == DIFFMPC_KERNEL_LATENCY || (sel == DIFFMPC_KERNEL_AUTO && p->B <= lat_max))) {
       auto lk = ilqr_forward_lat_kernel<M, DIAG, R>;
       if (LL.total > 48 * 1024) cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, LL.total);
       lk<<<p->B, kLatThreads, LL.total, s>>>(a);

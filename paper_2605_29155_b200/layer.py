@@ -27,7 +27,7 @@ class MpcSolver:
     """
 
     def __init__(self, model, settings, pool=None, mode="fused", n_slots=1, device=None,
-                 dtype=torch.float32):
+                 dtype=torch.float32, kernel="throughput"):
         if mode not in ("fused", "naive"):
             raise ConfigError(f"mode must be one of ('fused', 'naive'), got {mode!r}")
         self.model = model
@@ -37,6 +37,9 @@ class MpcSolver:
         self.n_slots = n_slots
         self.device = _solver._device(device)
         self.dtype = dtype
+        # One forward mapping for every batch size, so a minibatch re-solve reproduces the
+        # rollout's controls bit for bit (importance ratio exactly 1, trainer.py:9-12).
+        self.kernel = kernel
         u_min, u_max = settings.bounds_for(model.n_u)
         self.default_u = np.clip(model.hover_control(), u_min, u_max)
         self.warm = None
@@ -68,14 +71,15 @@ class MpcSolver:
         """
         dtype = dtype or self.dtype
         ws = _solver.solve_raw(self.model, self.settings, x_init, diag, cvec, U_warm, dtype=dtype,
-                               device=self.device)
+                               device=self.device, kernel=self.kernel)
         stats = {"dispatches_per_iteration": None, "total_dispatches": 1}
         return ws, ws.iters, ws.converged, ws.alpha_hist, stats
 
     def solve_dense(self, x_init, C, c, U_warm, dtype=None):
         """Dense-cost counterpart (batchexec.solve_raw, batchexec.py:156-163)."""
         dtype = dtype or self.dtype
-        ws = _solver.solve_raw(self.model, self.settings, x_init, C, c, U_warm, dtype=dtype, device=self.device)
+        ws = _solver.solve_raw(self.model, self.settings, x_init, C, c, U_warm, dtype=dtype, device=self.device,
+                               kernel=self.kernel)
         return ws, ws.iters, ws.converged, ws.alpha_hist, {"total_dispatches": 1}
 
 

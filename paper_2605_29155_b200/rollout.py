@@ -30,6 +30,7 @@ class DeviceRollout:
         self.u_lo = torch.as_tensor(bundle.u_min, dtype=torch.float64, device=self.device)
         self.u_hi = torch.as_tensor(bundle.u_max, dtype=torch.float64, device=self.device)
         self.step_count = 0
+        self.plan = None
 
     @torch.no_grad()
     def policy_means(self, obs_t):
@@ -38,9 +39,14 @@ class DeviceRollout:
         diag, cvec = self.bundle.actor(obs_t)
         x_init = self.env.mpc_state()
         U_warm = self.warm.clone()
-        ws, iterations, converged, _, _ = self.solver.solve_diag(x_init, diag, cvec, U_warm)
-        self.warm = torch.cat([ws.U[:, 1:], ws.U[:, -1:]], dim=1).to(torch.float32)
-        return ws.U[:, 0].to(torch.float32), x_init, U_warm, iterations
+        if self.plan is None:  # preallocated launch (the solve's outputs are consumed here)
+            from .solver import SolvePlan
+            self.plan = SolvePlan(self.solver.model, self.solver.settings, self.N, layout="diag",
+                                  dtype=torch.float32, device=self.device, want_gains=False, backward=False,
+                                  kernel=getattr(self.solver, "kernel", "throughput"))
+        ws = self.plan.solve(x_init.to(torch.float32).contiguous(), diag.contiguous(), cvec.contiguous(), U_warm)
+        self.warm = torch.cat([ws.U[:, 1:], ws.U[:, -1:]], dim=1)
+        return ws.U[:, 0].clone(), x_init, U_warm, ws.iters.clone()
 
     @torch.no_grad()
     def collect(self, steps: int | None = None):

@@ -114,10 +114,11 @@ class GradOutput:
 
 
 def solve_raw(model, settings, x_init, C, c, U_warm, *, dtype=torch.float32, device=None, theta=None,
-              stream=None, want_gains=True) -> SolveOutput:
+              stream=None, want_gains=True, kernel="auto") -> SolveOutput:
     """Batched iLQR solve over stacked cost arrays (batchexec.solve_raw, batchexec.py:156-163).
 
-    C is (B,T,nz,nz) dense or (B,T,nz) diagonal. One kernel launch.
+    C is (B,T,nz,nz) dense or (B,T,nz) diagonal. One kernel launch. ``kernel`` picks the
+    forward mapping ("auto" | "throughput" | "latency", see diffmpc.h kernel_select).
     """
     if dtype not in _DT:
         raise ConfigError(f"dtype must be float32 or float64, got {dtype}")
@@ -133,7 +134,7 @@ def solve_raw(model, settings, x_init, C, c, U_warm, *, dtype=torch.float32, dev
     c = _as(c, dtype, dev, (B, T, nz), "c")
     U_warm = _as(U_warm, dtype, dev, (B, T, nu), "U_warm")
     th, stride = _theta(model, theta, dtype, dev, B)
-    p = _abi.make_problem(model, settings, B, layout, stride)
+    p = _abi.make_problem(model, settings, B, layout, stride, kernel)
     f = dict(device=dev)
     out = SolveOutput(
         X=torch.empty((B, T + 1, nx), dtype=dtype, **f), U=torch.empty((B, T, nu), dtype=dtype, **f),
@@ -248,3 +249,93 @@ def dynamics_t(model, x, u, *, dtype=torch.float64, device=None, want_jac=False,
     with torch.cuda.device(dev):
         _lib.check(fn(ctypes.byref(p), N, P(th), P(x), P(u), P(xn), P(A), P(Bm), _stream()))
     return xn, A, Bm
+
+
+class SolvePlan:
+    """Preallocated forward (and backward) launches for a fixed problem shape.
+
+    ``solve_raw`` allocates its outputs and builds the ABI structs on every call (~0.1 ms of
+    host time — as much as a B=1 solve on the GPU). A plan does that once: outputs, gradient
+    buffers and the workspace are allocated up front, the ``DiffMPCProblem`` / IO structs are
+    filled once, and each call only patches the input pointers and enqueues the kernel(s).
+    Inputs must be contiguous device tensors of the plan's dtype and shapes; the returned
+    SolveOutput / GradOutput are the plan's own buffers (overwritten by the next call).
+    """
+
+    def __init__(self, model, settings, B, *, layout="dense", dtype=torch.float32, device=None, theta=None,
+                 want_gains=True, backward=True, kernel="auto"):
+        if dtype not in _DT:
+            raise ConfigError(f"dtype must be float32 or float64, got {dtype}")
+        self.dev = _device(device)
+        if self.dev.index is None:
+            self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.model, self.settings, self.B, self.dtype = model, settings, int(B), dtype
+        T, nx, nu = settings.T, model.n_x, model.n_u
+        nz = nx + nu
+        self.layout = _abi.COST_DENSE if layout == "dense" else _abi.COST_DIAG
+        self.C_shape = (self.B, T, nz, nz) if self.layout == _abi.COST_DENSE else (self.B, T, nz)
+        self.theta, stride = _theta(model, theta, dtype, self.dev, self.B)
+        self.p = _abi.make_problem(model, settings, self.B, self.layout, stride, kernel)
+        f = dict(device=self.dev)
+        self.out = SolveOutput(
+            X=torch.empty((B, T + 1, nx), dtype=dtype, **f), U=torch.empty((B, T, nu), dtype=dtype, **f),
+            J=torch.empty((B,), dtype=dtype, **f),
+            K=torch.empty((B, T, nu, nx), dtype=dtype, **f) if want_gains else None,
+            k=torch.empty((B, T, nu), dtype=dtype, **f) if want_gains else None,
+            iters=torch.empty((B,), dtype=torch.int32, **f), converged=torch.empty((B,), dtype=torch.uint8, **f),
+            diverged=torch.empty((B,), dtype=torch.uint8, **f), fail_t=torch.empty((B,), dtype=torch.int32, **f),
+            clamped=torch.empty((B, T, nu), dtype=torch.uint8, **f),
+            alpha_hist=torch.empty((B, settings.K_max), dtype=dtype, **f),
+            J_hist=torch.empty((B, settings.K_max + 1), dtype=dtype, **f), theta=self.theta, layout=self.layout)
+        L = _lib.lib()
+        P = _abi.ptr
+        wsb = int(L.diffmpc_forward_workspace_bytes(ctypes.byref(self.p), 4 if dtype == torch.float32 else 8))
+        self.ws = torch.empty((wsb,), dtype=torch.uint8, **f)
+        self.fio = _abi.DiffMPCForwardIO()
+        self.fio.theta = P(self.theta)
+        for name in ("X", "U", "J", "K", "k", "iters", "converged", "diverged", "fail_t", "clamped",
+                     "alpha_hist", "J_hist"):
+            setattr(self.fio, name, P(getattr(self.out, name)))
+        self.fio.workspace, self.fio.workspace_bytes = P(self.ws), wsb
+        self._fwd = getattr(L, f"diffmpc_forward_{_DT[dtype]}")
+        self.grad = None
+        if backward:
+            self.grad = GradOutput(dC=torch.empty(self.C_shape, dtype=dtype, **f),
+                                   dc=torch.empty((B, T, nz), dtype=dtype, **f),
+                                   dx0=torch.empty((B, nx), dtype=dtype, **f), dtheta=None,
+                                   fail_t=torch.empty((B,), dtype=torch.int32, **f))
+            self.bio = _abi.DiffMPCBackwardIO()
+            self.bio.theta = P(self.theta)
+            self.bio.dC, self.bio.dc, self.bio.dx0 = P(self.grad.dC), P(self.grad.dc), P(self.grad.dx0)
+            self.bio.fail_t = P(self.grad.fail_t)
+            self._bwd = getattr(L, f"diffmpc_backward_{_DT[dtype]}")
+
+    def _check(self, t, shape, name):
+        if (not isinstance(t, torch.Tensor) or t.dtype != self.dtype or t.device != self.dev
+                or tuple(t.shape) != tuple(shape) or not t.is_contiguous()):
+            raise ConfigError(f"{name}: expected a contiguous {self.dtype} tensor of shape {tuple(shape)} on {self.dev}")
+        return t.data_ptr()
+
+    def solve(self, x_init, C, c, U_warm, stream=None) -> SolveOutput:
+        T, nx, nu = self.settings.T, self.model.n_x, self.model.n_u
+        io = self.fio
+        io.x0 = self._check(x_init, (self.B, nx), "x_init")
+        io.C = self._check(C, self.C_shape, "C")
+        io.c = self._check(c, (self.B, T, nx + nu), "c")
+        io.U_warm = self._check(U_warm, (self.B, T, nu), "U_warm")
+        _lib.check(self._fwd(ctypes.byref(self.p), ctypes.byref(io), _stream(stream)))
+        self.out.C, self.out.c = C, c
+        return self.out
+
+    def backward(self, dLdX=None, dLdU=None, dLdJ=None, stream=None) -> GradOutput:
+        """Implicit backward at the last ``solve`` of this plan (its C, c, X, U)."""
+        if self.grad is None:
+            raise ConfigError("plan was built with backward=False")
+        T, nx, nu = self.settings.T, self.model.n_x, self.model.n_u
+        io, o = self.bio, self.out
+        io.C, io.c, io.X, io.U = o.C.data_ptr(), o.c.data_ptr(), o.X.data_ptr(), o.U.data_ptr()
+        io.dLdX = None if dLdX is None else self._check(dLdX, (self.B, T + 1, nx), "dL/dX")
+        io.dLdU = None if dLdU is None else self._check(dLdU, (self.B, T, nu), "dL/dU")
+        io.dLdJ = None if dLdJ is None else self._check(dLdJ, (self.B,), "dL/dJ")
+        _lib.check(self._bwd(ctypes.byref(self.p), ctypes.byref(io), _stream(stream)))
+        return self.grad

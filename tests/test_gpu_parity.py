@@ -160,3 +160,22 @@ np.savez(sys.argv[1], U=o.U.cpu().numpy(), X=o.X.cpu().numpy(), it=o.iters.cpu()
     np.testing.assert_array_equal(a["cl"], b["cl"])
     np.testing.assert_allclose(a["U"], b["U"], rtol=1e-4, atol=1e-4)
     np.testing.assert_allclose(a["J"], b["J"], rtol=1e-5)
+
+
+@pytest.mark.gpu
+def test_kernel_select_per_call():
+    """kernel_select picks the forward mapping per call; both agree on iterates, masks and
+    counts, and "throughput" is batch-size invariant bit for bit."""
+    from paper_2605_29155_b200 import DynModel, problems
+
+    m = DynModel.quadrotor()
+    pb = problems.random_problem(m, 64, 10, seed=33)
+    C = pb.dense_C()
+    lat = solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="latency")
+    tp = solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="throughput")
+    assert torch.equal(lat.iters, tp.iters) and torch.equal(lat.clamped, tp.clamped)
+    assert torch.allclose(lat.U, tp.U, rtol=1e-4, atol=1e-4)
+    one = solver.solve_raw(m, pb.settings, pb.x0[5:6], C[5:6], pb.c[5:6], pb.U_warm[5:6], kernel="throughput")
+    assert torch.equal(one.U[0], tp.U[5]) and torch.equal(one.X[0], tp.X[5])
+    with pytest.raises(Exception):
+        solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="fastest")

@@ -181,3 +181,26 @@ for i in range(30):
     assert torch.equal(a.X, ref.X) and torch.equal(a.K, ref.K) and torch.equal(a.iters, ref.iters), i
 '''
     subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=dict(os.environ, DIFFMPC_FWD="lat"))
+
+
+@pytest.mark.parametrize("layout", ["dense", "diag"])
+def test_solve_plan_matches_solve_raw(layout):
+    """The preallocated launch path gives the same results as the allocating API."""
+    m = DynModel.quadrotor()
+    pb = problems.random_problem(m, 40, 8, seed=5)
+    dev = torch.device("cuda")
+    C = pb.dense_C() if layout == "dense" else pb.diag
+    t = lambda a: torch.tensor(a, dtype=torch.float32, device=dev)  # noqa: E731
+    x0, Ct, c, Uw = t(pb.x0), t(C), t(pb.c), t(pb.U_warm)
+    ref = solver.solve_raw(m, pb.settings, x0, Ct, c, Uw)
+    dU = torch.zeros((40, 8, 4), device=dev)
+    dU[:, 0] = 1.0
+    gref = solver.backward_raw(m, pb.settings, Ct, c, ref.X, ref.U, None, dU)
+    plan = solver.SolvePlan(m, pb.settings, 40, layout=layout, device=dev)
+    for _ in range(2):  # reuse of the plan's buffers
+        out = plan.solve(x0, Ct, c, Uw)
+        g = plan.backward(dLdU=dU)
+        assert torch.equal(out.X, ref.X) and torch.equal(out.U, ref.U) and torch.equal(out.iters, ref.iters)
+        assert torch.equal(g.dC, gref.dC) and torch.equal(g.dc, gref.dc) and torch.equal(g.dx0, gref.dx0)
+    with pytest.raises(Exception):
+        plan.solve(x0.double(), Ct, c, Uw)
