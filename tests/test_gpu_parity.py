@@ -179,3 +179,27 @@ def test_kernel_select_per_call():
     assert torch.equal(one.U[0], tp.U[5]) and torch.equal(one.X[0], tp.X[5])
     with pytest.raises(Exception):
         solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="fastest")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alphas", [(1.0,), (1.0, 0.3), (1.0, 0.7, 0.5, 0.3, 0.2, 0.1), (1.0, 0.8, 0.6, 0.5, 0.4, 0.25, 0.1, 0.05)])
+@pytest.mark.parametrize("kernel", ["throughput", "latency"])
+def test_line_search_sizes_match_oracle(alphas, kernel):
+    """Step-size lists other than the default four: fewer candidates than the four slots
+    (duplicated slots) and two line-search rounds (five to eight candidates; no in-place
+    alpha_0 trajectory, winner re-rolled). f64 kernels vs the C oracle."""
+    import oracle
+    from paper_2605_29155_b200 import DynModel, problems
+
+    for model, B in ((DynModel.quadrotor(), 48), (DynModel.planar_quadrotor(dt=0.05), 64)):
+        pb = problems.random_problem(model, B, 8, seed=41, alphas=alphas)
+        C = pb.dense_C()
+        ref = oracle.forward(model, pb.settings, pb.x0, C, pb.c, pb.U_warm)
+        out = solver.solve_raw(model, pb.settings, pb.x0, C, pb.c, pb.U_warm, dtype=torch.float64, kernel=kernel)
+        np.testing.assert_array_equal(out.iters.cpu().numpy(), ref["iters"])
+        np.testing.assert_array_equal(out.clamped.cpu().numpy().astype(np.uint8),
+                                      ((ref["U"] <= pb.settings.bounds_for(model.n_u)[0]) |
+                                       (ref["U"] >= pb.settings.bounds_for(model.n_u)[1])).astype(np.uint8))
+        np.testing.assert_allclose(out.U.cpu().numpy(), ref["U"], rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(out.X.cpu().numpy(), ref["X"], rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(out.J.cpu().numpy(), ref["J"], rtol=1e-9)
