@@ -9,6 +9,8 @@ Public API (mirrors the reference package ``fusedmpc``):
                                                           one NCCL all-reduce, device-resident
                                                           rollouts, batched GPU race env)
     benchgrid                                           — latency grid in the bench CSV schema
+    api (solve, backward, solve_batch, backward_batch,  — object-level API of ilqr / gradlayer /
+         BatchProblem, make_hover_problem)                batchexec with the reference's errors
 Heavy modules (torch, the CUDA library) are imported lazily.
 """
 
