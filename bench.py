@@ -173,10 +173,14 @@ def run_ours(args):
     from paper_2605_29155_b200 import _lib, roofline, solver
 
     rank, world, local = dist_env()
+    # DIFFMPC_DRYRUN_SHARE_GPU=1: every rank on cuda:0 over gloo (exercises the multi-rank
+    # path on a one-GPU box; never used for reported numbers)
+    share = os.environ.get("DIFFMPC_DRYRUN_SHARE_GPU") == "1"
+    local = 0 if share else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("gloo" if share else "nccl", **({} if share else {"device_id": dev}))
     dtype = torch.float32 if args.dtype == "f32" else torch.float64
     pb = workload(args, seed=rank)
     model, st = pb.model, pb.settings

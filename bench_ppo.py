@@ -51,10 +51,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DIFFMPC_DRYRUN_SHARE_GPU=1: every rank on cuda:0 over gloo (exercises the multi-rank
+    # path on a one-GPU box; never used for reported numbers)
+    share = os.environ.get("DIFFMPC_DRYRUN_SHARE_GPU") == "1"
+    local = 0 if share else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("gloo" if share else "nccl", **({} if share else {"device_id": dev}))
     B, T = args.minibatch, args.T
     model = DynModel.quadrotor(dt=0.05)
     pb = problems.hover_problem(model, B, T, seed=100 + rank)
@@ -128,10 +132,14 @@ def train_mode(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DIFFMPC_DRYRUN_SHARE_GPU=1: every rank on cuda:0 over gloo (exercises the multi-rank
+    # path on a one-GPU box; never used for reported numbers)
+    share = os.environ.get("DIFFMPC_DRYRUN_SHARE_GPU") == "1"
+    local = 0 if share else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("gloo" if share else "nccl", **({} if share else {"device_id": dev}))
     model = DynModel.planar_quadrotor(dt=0.05)
     st = SolveSettings(T=args.T, u_min=0.0, u_max=2 * 0.5 * 9.81)
     torch.manual_seed(0)
