@@ -248,7 +248,7 @@ def run_ours(args):
     # results device->host. Steps are issued round-robin on NS streams so the H2D copy of
     # step k+1, the kernels of step k and the D2H copy of step k-1 overlap (the two PCIe
     # directions run on separate copy engines), as a serving loop would stream batches.
-    NS = 3
+    NS = int(os.environ.get("DIFFMPC_E2E_STREAMS", "3"))
     streams = [torch.cuda.Stream(device=dev) for _ in range(NS)]
     res_host = [{"U": torch.empty((B, T, m), dtype=dtype).pin_memory(),
                  "J": torch.empty((B,), dtype=dtype).pin_memory(),
