@@ -203,3 +203,23 @@ def test_line_search_sizes_match_oracle(alphas, kernel):
         np.testing.assert_allclose(out.U.cpu().numpy(), ref["U"], rtol=1e-9, atol=1e-9)
         np.testing.assert_allclose(out.X.cpu().numpy(), ref["X"], rtol=1e-9, atol=1e-9)
         np.testing.assert_allclose(out.J.cpu().numpy(), ref["J"], rtol=1e-9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,T", [(1, 3), (3, 10), (33, 10), (17, 40)])
+@pytest.mark.parametrize("kernel", ["throughput", "latency"])
+def test_odd_batches_and_long_horizons_match_oracle(B, T, kernel):
+    """Batch sizes that do not fill a warp pair / block, and T=40 (largest per-problem shared
+    memory), against the oracle in float64."""
+    import oracle
+    from paper_2605_29155_b200 import DynModel, problems
+
+    m = DynModel.quadrotor()
+    pb = problems.random_problem(m, B, T, seed=B * 100 + T)
+    C = pb.dense_C()
+    ref = oracle.forward(m, pb.settings, pb.x0, C, pb.c, pb.U_warm)
+    out = solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, dtype=torch.float64, kernel=kernel)
+    np.testing.assert_array_equal(out.iters.cpu().numpy(), ref["iters"])
+    np.testing.assert_allclose(out.U.cpu().numpy(), ref["U"], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(out.J.cpu().numpy(), ref["J"], rtol=1e-9)
+    np.testing.assert_allclose(out.K.cpu().numpy(), ref["K"], rtol=1e-7, atol=1e-9)
