@@ -260,6 +260,64 @@ struct Quad13 {
     A[11 * lda + 10] = ey * (dxz * wz); A[11 * lda + 12] = ey * (dxz * wx);
     A[12 * lda + 10] = ez * (dyx * wy); A[12 * lda + 11] = ez * (dyx * wx);
   }
+  // Register-resident rows of A_t / B_t for the Riccati products: the 23 distinct
+  // state-dependent values of one stage (same arithmetic as jac_vary / jac_const, so the
+  // rows are bit-identical to the shared-memory copy) and a row accessor that the products
+  // call with compile-time row indices (after unrolling), replacing shared-memory row loads.
+  template <class S>
+  struct JacRegs {
+    S hwW[3], hwQ[4], dq[4], g[6], b[6];  // b: B rows 7..9 (b7,b8,b9) and 10..12 (bx,by,bz)
+  };
+  template <class S>
+  DMPC_DEV static void jac_regs(const S* P, S dt, const S* z, JacRegs<S>& J) {
+    const S im = P[7], iJx = P[9], iJy = P[10], iJz = P[11];
+    const S dzy = P[12], dxz = P[13], dyx = P[14];
+    const S qw = z[3], qx = z[4], qy = z[5], qz = z[6];
+    const S wx = z[10], wy = z[11], wz = z[12];
+    const S F = ((z[13] + z[14]) + z[15]) + z[16];
+    const S hw = S(0.5) * dt;
+    const S da = dt * (F * im);
+    J.hwW[0] = hw * wx; J.hwW[1] = hw * wy; J.hwW[2] = hw * wz;
+    J.hwQ[0] = hw * qw; J.hwQ[1] = hw * qx; J.hwQ[2] = hw * qy; J.hwQ[3] = hw * qz;
+    J.dq[0] = da * (S(2) * qw); J.dq[1] = da * (S(2) * qx); J.dq[2] = da * (S(2) * qy); J.dq[3] = da * (S(2) * qz);
+    const S ex = -dt * iJx, ey = -dt * iJy, ez = -dt * iJz;
+    J.g[0] = ex * (dzy * wz); J.g[1] = ex * (dzy * wy); J.g[2] = ey * (dxz * wz);
+    J.g[3] = ey * (dxz * wx); J.g[4] = ez * (dyx * wy); J.g[5] = ez * (dyx * wx);
+    const S dm = dt * im;
+    J.b[0] = (S(2) * (qx * qz + qw * qy)) * dm;
+    J.b[1] = (S(2) * (qy * qz - qw * qx)) * dm;
+    J.b[2] = (S(1) - S(2) * (qx * qx + qy * qy)) * dm;
+    J.b[3] = dt * P[8] * P[9];
+    J.b[4] = dt * P[8] * P[10];
+    J.b[5] = dt * P[5] * P[11];
+  }
+  // state-dependent entries of A row r (others are unused by the callers) and B row r
+  template <class S>
+  DMPC_DEV static void jac_row(const JacRegs<S>& J, int r, S (&a)[NX], S (&b)[NU]) {
+    switch (r) {
+      case 3: a[4] = -J.hwW[0]; a[5] = -J.hwW[1]; a[6] = -J.hwW[2];
+              a[10] = -J.hwQ[1]; a[11] = -J.hwQ[2]; a[12] = -J.hwQ[3]; break;
+      case 4: a[3] = J.hwW[0]; a[5] = J.hwW[2]; a[6] = -J.hwW[1];
+              a[10] = J.hwQ[0]; a[11] = -J.hwQ[3]; a[12] = J.hwQ[2]; break;
+      case 5: a[3] = J.hwW[1]; a[4] = -J.hwW[2]; a[6] = J.hwW[0];
+              a[10] = J.hwQ[3]; a[11] = J.hwQ[0]; a[12] = -J.hwQ[1]; break;
+      case 6: a[3] = J.hwW[2]; a[4] = J.hwW[1]; a[5] = -J.hwW[0];
+              a[10] = -J.hwQ[2]; a[11] = J.hwQ[1]; a[12] = J.hwQ[0]; break;
+      case 7: a[3] = J.dq[2]; a[4] = J.dq[3]; a[5] = J.dq[0]; a[6] = J.dq[1];
+              b[0] = b[1] = b[2] = b[3] = J.b[0]; break;
+      case 8: a[3] = -J.dq[1]; a[4] = -J.dq[0]; a[5] = J.dq[3]; a[6] = J.dq[2];
+              b[0] = b[1] = b[2] = b[3] = J.b[1]; break;
+      case 9: a[4] = S(-2) * J.dq[1]; a[5] = S(-2) * J.dq[2];
+              b[0] = b[1] = b[2] = b[3] = J.b[2]; break;
+      case 10: a[11] = J.g[0]; a[12] = J.g[1];
+               b[0] = J.b[3]; b[1] = J.b[3]; b[2] = -J.b[3]; b[3] = -J.b[3]; break;
+      case 11: a[10] = J.g[2]; a[12] = J.g[3];
+               b[0] = -J.b[4]; b[1] = J.b[4]; b[2] = J.b[4]; b[3] = -J.b[4]; break;
+      case 12: a[10] = J.g[4]; a[11] = J.g[5];
+               b[0] = J.b[5]; b[1] = -J.b[5]; b[2] = J.b[5]; b[3] = -J.b[5]; break;
+      default: break;
+    }
+  }
   template <class S>
   DMPC_DEV static void theta_grad(const S* P, S dt, const S* x, const S* u, const S* dx,
                                   const S* du, const S* lh, const S* lam, S* g) {

@@ -8,6 +8,8 @@
 // fetched with 128-bit broadcast loads (LDS.128): the row-lane products issue one
 // vector load per 4 (f32) FMAs instead of one scalar load per FMA.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace dmpc {
@@ -243,11 +245,32 @@ __host__ __device__ constexpr bool b_row_nz(int r) {
   return any;
 }
 
+// Row providers of A_t / B_t for the products: the shared-memory copy (any model), or
+// register-resident rows formed from a model's per-stage JacRegs (no shared-memory loads).
+template <class M, bool DIAG, class R>
+struct SmemRows {
+  const Ric<M, DIAG, R>& S;
+  DMPC_DEV void get(int r, R (&a)[M::NX], R (&b)[M::NU]) const {
+    using D = Dims<M, DIAG, R>;
+    if (a_row_sd<M>(r)) lds_row<M::NX>(S.As + r * D::LDA, a);
+    if (b_row_nz<M>(r)) lds_row<M::NU>(S.Bs + r * D::LDB, b);
+  }
+};
+template <class M, class R>
+struct RegRows {
+  typename M::template JacRegs<R> J;
+  DMPC_DEV void get(int r, R (&a)[M::NX], R (&b)[M::NU]) const { M::template jac_row<R>(J, r, a, b); }
+};
+template <class M, class = void>
+struct has_jac_regs : std::false_type {};
+template <class M>
+struct has_jac_regs<M, std::void_t<typename M::template JacRegs<float>>> : std::true_type {};
+
 // MA = V_xx A, NB = V_xx B  (kernels.py:411-421 / 629-639). Terms on structural zeros of
 // A_t / B_t (M::a_nz / M::b_nz, compile-time) are skipped; the row of A is the same for
 // every lane, so the skipping is uniform (no divergence).
-template <class M, bool DIAG, class R, int G, int RPL>
-DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][M::NX], R dt) {
+template <class M, bool DIAG, class R, int G, int RPL, class Rows>
+DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][M::NX], R dt, const Rows& rows) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
   R ma[RPL][NX], nb[RPL][NU];
@@ -261,8 +284,7 @@ DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][
 #pragma unroll
   for (int r = 0; r < NX; r++) {
     R arow[NX], brow[NU];
-    if (a_row_sd<M>(r)) lds_row<NX>(S.As + r * D::LDA, arow);
-    if (b_row_nz<M>(r)) lds_row<NU>(S.Bs + r * D::LDB, brow);
+    rows.get(r, arow, brow);
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
       const R v = vxx[k][r];
@@ -293,9 +315,9 @@ DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][
 // C_ux[:,a] + sum_r B[r,:] MA[r,a] (kernels.py:428-433). A' V_xx A is evaluated as
 // MA' A (V_xx is exactly symmetric), i.e. row a = sum_r MA[r,a] A[r,:]: the lane-uniform
 // operand is again a row of A, so its structural zeros are skipped without divergence.
-template <class M, bool DIAG, class R, int G, int RPL>
+template <class M, bool DIAG, class R, int G, int RPL, class Rows>
 DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&qxx)[RPL][M::NX],
-                          R (&quxc)[RPL][M::NU], R dt) {
+                          R (&quxc)[RPL][M::NU], R dt, const Rows& rows) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
   int ac[RPL];  // clamped row index (padding rows alias the last row; never stored)
@@ -318,8 +340,7 @@ DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&q
 #pragma unroll
   for (int r = 0; r < NX; r++) {
     R arow[NX], brow[NU];
-    if (a_row_sd<M>(r)) lds_row<NX>(S.As + r * D::LDA, arow);
-    if (b_row_nz<M>(r)) lds_row<NU>(S.Bs + r * D::LDB, brow);
+    rows.get(r, arow, brow);
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
       const R mra = S.MA[r * D::LDA + ac[k]];
