@@ -182,11 +182,33 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         for (int b2 = 0; b2 < NX; b2++) s += S.Bs[b2 * LDB + a] * vx[b2];
         S.qu[a] = s;
       }
-      ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, SmemRows<M, DIAG, R>{S});
+      if constexpr (has_jac_regs<M>::value) {
+        R zr[NZ];
+#pragma unroll
+        for (int i = 0; i < NX; i++) zr[i] = xr[i];
+#pragma unroll
+        for (int i = 0; i < NU; i++) zr[NX + i] = ur[i];
+        RegRows<M, R> rr;
+        M::template jac_regs<R>(P_r, dt_r, zr, rr.J);
+        ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rr);
+      } else {
+        ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, SmemRows<M, DIAG, R>{S});
+      }
       __syncwarp(gm);
       for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU);
       R quxc[RPL][NU], qxx[RPL][NX];
-      ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, SmemRows<M, DIAG, R>{S});
+      if constexpr (has_jac_regs<M>::value) {
+        R zr[NZ];
+#pragma unroll
+        for (int i = 0; i < NX; i++) zr[i] = xr[i];
+#pragma unroll
+        for (int i = 0; i < NU; i++) zr[NX + i] = ur[i];
+        RegRows<M, R> rr;
+        M::template jac_regs<R>(P_r, dt_r, zr, rr.J);
+        ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, rr);
+      } else {
+        ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, SmemRows<M, DIAG, R>{S});
+      }
       __syncwarp(gm);
       ricp.release(t);
       // freeze clamped dimensions (kernels.py:658-667)
