@@ -369,7 +369,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       __syncwarp(gm);  // previous stage done with As/Bs/MA; z_t and the staging visible
       R zv[NZ], vx[NX];
       lds_row<NZ>(S.zs, zv);
-      if constexpr (!M::kLinearParams) {
+      // stage Jacobian values once: register rows for the products, plus the shared copy
+      // of the state-dependent entries for the column accesses (A'Vx, B'NB)
+      using Rows = std::conditional_t<has_jac_regs<M>::value, RegRows<M, R>, SmemRows<M, DIAG, R>>;
+      Rows rows = make_rows<M, DIAG, R>(S, P_r, dt_r, zv);
+      if constexpr (has_jac_regs<M>::value) {
+        jac_store_rows<M, R>(rows, S.As, LDA, S.Bs, LDB);
+      } else if constexpr (!M::kLinearParams) {
         R xr[NX], ur[NU];
 #pragma unroll
         for (int i = 0; i < NX; i++) xr[i] = zv[i];
@@ -412,23 +418,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           if (b_row_nz<M>(b2)) sa[2 + (b2 & 1)] += S.Bs[b2 * LDB + a] * vx[b2];
         S.qu[a] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
       }
-      if constexpr (has_jac_regs<M>::value) {
-        RegRows<M, R> rr;
-        M::template jac_regs<R>(P_r, dt_r, zv, rr.J);
-        ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rr);
-      } else {
-        ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, SmemRows<M, DIAG, R>{S});
-      }
+      ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rows);
       __syncwarp(gm);
       for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU);
       R quxc[RPL][NU], qxx[RPL][NX];
-      if constexpr (has_jac_regs<M>::value) {
-        RegRows<M, R> rr;
-        M::template jac_regs<R>(P_r, dt_r, zv, rr.J);
-        ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, rr);
-      } else {
-        ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, SmemRows<M, DIAG, R>{S});
-      }
+      ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, rows);
       __syncwarp(gm);
       bwdp.release(t);  // C_t fully consumed: prefetch C_{t-1}
       // ---- stage QP on the control increment (type R, all lanes redundantly) ----

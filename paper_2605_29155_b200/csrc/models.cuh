@@ -291,6 +291,9 @@ struct Quad13 {
     J.b[4] = dt * P[8] * P[10];
     J.b[5] = dt * P[5] * P[11];
   }
+  // rows of B_t that change with the state (7..9; rows 10..12 are constant, jac_const)
+  template <int Dummy>
+  __host__ __device__ static constexpr bool b_varies(int r) { return r >= 7 && r <= 9; }
   // state-dependent entries of A row r (others are unused by the callers) and B row r
   template <class S>
   DMPC_DEV static void jac_row(const JacRegs<S>& J, int r, S (&a)[NX], S (&b)[NU]) {

@@ -261,10 +261,40 @@ struct RegRows {
   typename M::template JacRegs<R> J;
   DMPC_DEV void get(int r, R (&a)[M::NX], R (&b)[M::NU]) const { M::template jac_row<R>(J, r, a, b); }
 };
+// Write the state-dependent entries of A_t (and the rows of B_t) held in a RegRows to the
+// shared-memory copy (the consumers that need columns of A / B read that copy); the values
+// are the ones jac_vary would store.
+template <class M, class R, class J>
+DMPC_DEV void jac_store_rows(const J& rows, R* A, int lda, R* B, int ldb) {
+#pragma unroll
+  for (int r = 0; r < M::NX; r++) {
+    R a[M::NX], b[M::NU];
+    rows.get(r, a, b);
+#pragma unroll
+    for (int c = 0; c < M::NX; c++)
+      if (M::a_nz(r, c) && !M::a_one(r, c) && !M::a_dt(r, c)) A[r * lda + c] = a[c];
+    if (M::template b_varies<0>(r)) {
+#pragma unroll
+      for (int c = 0; c < M::NU; c++) B[r * ldb + c] = b[c];
+    }
+  }
+}
+
 template <class M, class = void>
 struct has_jac_regs : std::false_type {};
 template <class M>
 struct has_jac_regs<M, std::void_t<typename M::template JacRegs<float>>> : std::true_type {};
+
+template <class M, bool DIAG, class R, class Z>
+DMPC_DEV auto make_rows(const Ric<M, DIAG, R>& S, const R* P, R dt, const Z& z) {
+  if constexpr (has_jac_regs<M>::value) {
+    RegRows<M, R> rr;
+    M::template jac_regs<R>(P, dt, z, rr.J);
+    return rr;
+  } else {
+    return SmemRows<M, DIAG, R>{S};
+  }
+}
 
 // MA = V_xx A, NB = V_xx B  (kernels.py:411-421 / 629-639). Terms on structural zeros of
 // A_t / B_t (M::a_nz / M::b_nz, compile-time) are skipped; the row of A is the same for
