@@ -162,8 +162,20 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       R xr[NX], ur[NU];
       lds_row<NX>(Xs + t * LDA, xr);
       lds_row<NU>(Us + t * LDB, ur);
+      R zr[NZ];
+#pragma unroll
+      for (int i = 0; i < NX; i++) zr[i] = xr[i];
+#pragma unroll
+      for (int i = 0; i < NU; i++) zr[NX + i] = ur[i];
       __syncwarp(gm);
-      if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
+      // stage Jacobian values once (register rows + the shared copy for column accesses)
+      using Rows = std::conditional_t<has_jac_regs<M>::value, RegRows<M, R>, SmemRows<M, DIAG, R>>;
+      Rows rows = make_rows<M, DIAG, R>(S, P_r, dt_r, zr);
+      if constexpr (has_jac_regs<M>::value) {
+        jac_store_rows<M, R>(rows, S.As, LDA, S.Bs, LDB);
+      } else if constexpr (!M::kLinearParams) {
+        M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
+      }
       __syncwarp(gm);
       R qx[RPL];
       R vx[NX];
@@ -182,33 +194,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         for (int b2 = 0; b2 < NX; b2++) s += S.Bs[b2 * LDB + a] * vx[b2];
         S.qu[a] = s;
       }
-      if constexpr (has_jac_regs<M>::value) {
-        R zr[NZ];
-#pragma unroll
-        for (int i = 0; i < NX; i++) zr[i] = xr[i];
-#pragma unroll
-        for (int i = 0; i < NU; i++) zr[NX + i] = ur[i];
-        RegRows<M, R> rr;
-        M::template jac_regs<R>(P_r, dt_r, zr, rr.J);
-        ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rr);
-      } else {
-        ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, SmemRows<M, DIAG, R>{S});
-      }
+      ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rows);
       __syncwarp(gm);
       for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU);
       R quxc[RPL][NU], qxx[RPL][NX];
-      if constexpr (has_jac_regs<M>::value) {
-        R zr[NZ];
-#pragma unroll
-        for (int i = 0; i < NX; i++) zr[i] = xr[i];
-#pragma unroll
-        for (int i = 0; i < NU; i++) zr[NX + i] = ur[i];
-        RegRows<M, R> rr;
-        M::template jac_regs<R>(P_r, dt_r, zr, rr.J);
-        ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, rr);
-      } else {
-        ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, SmemRows<M, DIAG, R>{S});
-      }
+      ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, rows);
       __syncwarp(gm);
       ricp.release(t);
       // freeze clamped dimensions (kernels.py:658-667)
