@@ -29,10 +29,9 @@
 // global workspace ([problem][t][n_u][LDA], written by the sweep, streamed back per
 // stage by the line search), which keeps ~8.5 KB of shared memory per 13-state problem.
 //
-// Scheduling: a persistent grid (resident blocks only). Each warp claims the next
-// 32/G problems with one atomicAdd on a per-launch counter and solves them in lockstep;
-// a warp whose problems converge early claims more work instead of idling until the
-// slowest problem of its block is done.
+// Scheduling: a persistent grid (resident blocks only). Each G-lane group claims its next
+// problem with one atomicAdd on a per-launch counter; a group whose problem converges early
+// claims more work instead of idling until the slowest problem of its block is done.
 #pragma once
 #include <type_traits>
 
@@ -65,8 +64,6 @@ struct FwdArgs {
   void* Pw;            // packed cost records (B, T, REC) of R
   long long kw_stride, pw_stride;  // per-problem workspace strides (elements of R, 128-byte multiples)
   int* ctr;            // per-launch work counter (zeroed before the launch)
-  int pw;              // problems per warp claimed by one atomicAdd (32/G, or gpb if smaller)
-  int claim_group;     // 1: each group claims its own problems (DIFFMPC_CLAIM=group)
 };
 
 __host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a * a; }
@@ -145,11 +142,6 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   const int lane = threadIdx.x % G;
   if (grp >= args.gpb) return;
   const unsigned gm = group_mask<G>();
-  // warp-level work claiming: the warp's `pw` groups take consecutive problems
-  const int pw = args.pw;
-  const int wlanes = pw * G;  // live lanes of this warp
-  const unsigned wmask = wlanes >= 32 ? 0xffffffffu : ((1u << wlanes) - 1u);
-  const int gi = (threadIdx.x & 31) / G;  // group index within the warp
   const int T = args.T;
   const Lay L = Lay::make(T);
   unsigned char* base = smem_raw + (size_t)grp * args.smem_stride;
@@ -160,24 +152,17 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   R* Kb = (R*)(base + L.oKb);
   Ric<M, DIAG, R> S;
   S.bind(base, L.ric);
-  // per_group: every group claims its own next problem (the groups of a warp then run
-  // independent instruction streams); otherwise the warp's groups claim together
-  const bool per_group = args.claim_group != 0;
-  const int upw = per_group ? 1 : pw;
-  const int units = (args.B + upw - 1) / upw;
-
+  // Every group claims its own next problem with one atomicAdd by its lane 0 and a
+  // group-masked broadcast. (A warp-wide claim — one full-mask shuffle reached by the two
+  // groups of a warp at different times, while the other group executes group-masked
+  // collectives — intermittently lost the second group's problem; tools/stress_b7.py.)
   auto claim = [&]() -> int {
     int u = 0;
-    if (per_group) {
-      if (lane == 0) u = atomicAdd(args.ctr, 1);
-      return __shfl_sync(gm, u, 0, G);
-    }
-    if ((threadIdx.x & 31) == 0) u = atomicAdd(args.ctr, 1);
-    return __shfl_sync(wmask, u, 0);
+    if (lane == 0) u = atomicAdd(args.ctr, 1);
+    return __shfl_sync(gm, u, 0, G);
   };
 
-  for (int unit = claim(); unit < units; unit = claim()) {
-  const int pid = per_group ? unit : unit * pw + gi;
+  for (int pid = claim(); pid < args.B; pid = claim()) {
   if (pid < args.B) {
   double* Un = Ubuf0;  // nominal controls (swapped with the alpha_0 candidate's on accept)
   double* Us = Ubuf1;

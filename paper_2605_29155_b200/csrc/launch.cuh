@@ -143,18 +143,9 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
     while (g < p->B) g *= 2;
     a.gpb = g;
   }
-  a.pw = (32 / G < a.gpb) ? 32 / G : a.gpb;
-  {
-    static int cg = -1;
-    if (cg < 0) {
-      const char* e = getenv("DIFFMPC_CLAIM");
-      cg = (e && std::string(e) == "group") ? 1 : 0;
-    }
-    a.claim_group = cg;
-  }
   const int smem = a.gpb * a.smem_stride;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  // persistent grid: at most the resident blocks; warps claim problems dynamically
+  // persistent grid: at most the resident blocks; groups claim problems dynamically
   const int need_blocks = (p->B + a.gpb - 1) / a.gpb;
   const int resident = per_sm * num_sms();
   const int blocks = need_blocks < resident ? need_blocks : resident;

@@ -204,3 +204,17 @@ def test_solve_plan_matches_solve_raw(layout):
         assert torch.equal(g.dC, gref.dC) and torch.equal(g.dc, gref.dc) and torch.equal(g.dx0, gref.dx0)
     with pytest.raises(Exception):
         plan.solve(x0.double(), Ct, c, Uw)
+
+
+@pytest.mark.parametrize("B", [3, 5, 7, 33])
+def test_small_odd_batches_repeatable(B):
+    """Every problem of small odd batches is solved and written on every launch (regression
+    test for the warp-level work claim that intermittently dropped a warp's second group)."""
+    m = DynModel.quadrotor()
+    pb = problems.random_problem(m, B, 10, seed=B)
+    C = pb.dense_C()
+    ref = solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="throughput")
+    assert bool(((ref.iters >= 1) & (ref.iters <= pb.settings.K_max)).all())
+    for _ in range(25):
+        o = solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="throughput")
+        assert torch.equal(o.iters, ref.iters) and torch.equal(o.U, ref.U) and torch.equal(o.J, ref.J)
