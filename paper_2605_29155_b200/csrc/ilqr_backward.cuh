@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       }
       ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rows);
       __syncwarp(gm);
-      for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU);
+      for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU, rows);
       R quxc[RPL][NU], qxx[RPL][NX];
       ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, rows);
       __syncwarp(gm);

@@ -321,6 +321,19 @@ struct Quad13 {
       default: break;
     }
   }
+  // B[r][i] with a runtime column i (rows 7..9 are column-uniform, 10..12 the X mixer signs)
+  template <class S>
+  DMPC_DEV static S jac_b(const JacRegs<S>& J, int r, int i) {
+    switch (r) {
+      case 7: return J.b[0];
+      case 8: return J.b[1];
+      case 9: return J.b[2];
+      case 10: return i < 2 ? J.b[3] : -J.b[3];
+      case 11: return (i == 1 || i == 2) ? J.b[4] : -J.b[4];
+      case 12: return (i & 1) ? -J.b[5] : J.b[5];
+      default: return S(0);
+    }
+  }
   template <class S>
   DMPC_DEV static void theta_grad(const S* P, S dt, const S* x, const S* u, const S* dx,
                                   const S* du, const S* lh, const S* lam, S* g) {

@@ -255,11 +255,13 @@ struct SmemRows {
     if (a_row_sd<M>(r)) lds_row<M::NX>(S.As + r * D::LDA, a);
     if (b_row_nz<M>(r)) lds_row<M::NU>(S.Bs + r * D::LDB, b);
   }
+  DMPC_DEV R b(int r, int i) const { return S.Bs[r * Dims<M, DIAG, R>::LDB + i]; }  // B[r][i]
 };
 template <class M, class R>
 struct RegRows {
   typename M::template JacRegs<R> J;
   DMPC_DEV void get(int r, R (&a)[M::NX], R (&b)[M::NU]) const { M::template jac_row<R>(J, r, a, b); }
+  DMPC_DEV R b(int r, int i) const { return M::template jac_b<R>(J, r, i); }  // B[r][i], runtime column
 };
 // Write the state-dependent entries of A_t (and the rows of B_t) held in a RegRows to the
 // shared-memory copy (the consumers that need columns of A / B read that copy); the values
@@ -388,8 +390,8 @@ DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&q
 }
 
 // Q_uu entry (i,j) = C_uu[i,j] + sum_r B[r,i] NB[r,j]  (kernels.py:434-439)
-template <class M, bool DIAG, class R>
-DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j) {
+template <class M, bool DIAG, class R, class Rows>
+DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j, const Rows& rows) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX;
   R s;
@@ -400,7 +402,7 @@ DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j) {
   }
 #pragma unroll
   for (int r = 0; r < NX; r++)
-    if (b_row_nz<M>(r)) s += S.Bs[r * D::LDB + i] * S.NB[r * D::LDB + j];
+    if (b_row_nz<M>(r)) s += rows.b(r, i) * S.NB[r * D::LDB + j];
   return s;
 }
 
