@@ -294,6 +294,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = world * B / (e2e_ms * 1e-3)
+    pcie = pcie_bidir_gbs(dev)  # both copy directions at once: the bound of the e2e leg
 
     # ---- latency path (BASELINE config 2): forward-only at B=1 and B=256 ----
     lat = {}
@@ -326,6 +327,28 @@ def run_ours(args):
             lat[f"b{Bl}_per_iter_us"] = round(1e3 * ms / max(1, mx), 2)
             lat[f"b{Bl}_sync_call_ms"] = round(wall, 4)
 
+    # ---- fixed work: conv_tol = 0, every problem runs K_max iterations ----
+    import dataclasses
+    st0 = dataclasses.replace(st, conv_tol=0.0)
+    fx = []
+    for k in range(3 + 10):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        o0 = solver.solve_raw(model, st0, dev_in["x0"], dev_in["C"], dev_in["c"], dev_in["U_warm"], dtype=dtype)
+        e1.record(stream)
+        solver.backward_raw(model, st0, dev_in["C"], dev_in["c"], o0.X, o0.U, None, dev_in["dLdU"], dtype=dtype)
+        e2.record(stream)
+        if k >= 3:
+            fx.append((e0, e1, e2))
+    torch.cuda.synchronize()
+    fx_f = float(np.median([a.elapsed_time(b) for a, b, _ in fx]))
+    fx_b = float(np.median([b.elapsed_time(c) for _, b, c in fx]))
+    it0 = o0.iters.cpu().numpy()
+    fixed = {"value": world * B / ((fx_f + fx_b) * 1e-3), "unit": "solves/s", "forward_ms": fx_f,
+             "backward_ms": fx_b, "mean_iters": float(it0.mean()),
+             "fwd_tflops": roofline.fwd_flops(n, m, T, it0, len(st.alphas)) / (fx_f * 1e-3) / 1e12,
+             "how": "conv_tol=0, K_max=10, same inputs; per-rank device time, median of 10"}
+
     # ---- roofline of the dominant kernel (the fused forward) ----
     F = roofline.fwd_flops(n, m, T, it_np, len(st.alphas))
     achieved = F / (fwd_ms * 1e-3) / 1e12
@@ -346,13 +369,17 @@ def run_ours(args):
                 "config": config(args, world),
                 "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-                        "pipeline": f"{NS} streams round-robin (H2D / kernels / D2H overlap)"},
+                        "pipeline": f"{NS} streams round-robin (H2D / kernels / D2H overlap)",
+                        "pcie_bound": {"bidir_gbs": pcie, "bound_ms": (h2d + d2h) / (pcie * 1e6),
+                                       "frac": (h2d + d2h) / (pcie * 1e6) / e2e_ms,
+                                       "how": "64 MB pinned H2D + D2H concurrently on two streams, median of 5"}},
                 "gpu_launches": int(gpu_launches),
                 "launches_per_step": gpu_launches / args.steps,
                 "launches_per_ilqr_iteration": (gpu_launches / args.steps - 1) / float(iters.max().item()),
                 "forward_ms": fwd_ms, "backward_ms": bwd_ms,
                 "mean_iters": float(iters.mean().item()), "max_iters": int(iters.max().item()),
                 "latency": lat,
+                "fixed_work": dict(fixed, roofline_frac=fixed["fwd_tflops"] / peak),
                 "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "traffic": traffic, "kernel": "ilqr_forward_kernel",
                              "peak_source": peak_kind,
@@ -367,6 +394,33 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def pcie_bidir_gbs(dev, mb=64, reps=5):
+    """Host<->device copy bandwidth with both directions busy (tools/pcie_probe.py)."""
+    import torch
+
+    n = mb << 20
+    h_in, h_out = torch.empty(n, dtype=torch.uint8).pin_memory(), torch.empty(n, dtype=torch.uint8).pin_memory()
+    d_in, d_out = torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2, main = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev), torch.cuda.current_stream(dev)
+    ts = []
+    for i in range(reps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a.record(main)
+        for s, (dst, src) in ((s1, (d_in, h_in)), (s2, (h_out, d_out))):
+            s.wait_event(a)
+            with torch.cuda.stream(s):
+                dst.copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s)
+            main.wait_event(ev)
+        b.record(main)
+        torch.cuda.synchronize(dev)
+        if i:
+            ts.append(a.elapsed_time(b))
+    return 2 * n / float(np.median(ts)) / 1e6
 
 
 def fp32_peak(dev):

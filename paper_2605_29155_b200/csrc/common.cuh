@@ -59,12 +59,6 @@ DMPC_DEV void cp_async_16cg(void* dst, const void* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
-// Drop one 128-byte L2 line without writing it back (its contents become undefined):
-// used on the workspace of a finished problem, which is never read again.
-DMPC_DEV void l2_discard(const void* p) {
-  asm volatile("{\n\t.reg .u64 ga;\n\tcvta.to.global.u64 ga, %0;\n\tdiscard.global.L2 [ga], 128;\n\t}\n" ::"l"(p)
-               : "memory");
-}
 DMPC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 DMPC_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 

@@ -127,7 +127,7 @@ DMPC_DEV double feedback(double v, const R (&krow)[NX], const double (&x)[NX], c
   return v + v1;
 }
 
-template <class M, int G, bool DIAG, class R>
+template <class M, int G, bool DIAG, class R, bool LOCK>
 __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (DIAG || M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   const int grp = threadIdx.x / G;
   const int lane = threadIdx.x % G;
   if (grp >= args.gpb) return;
+  const unsigned wm = __activemask();  // the warp's groups (kernel entry: converged)
   const unsigned gm = group_mask<G>();
   const int T = args.T;
   const Lay L = Lay::make(T);
@@ -162,8 +163,23 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     return __shfl_sync(gm, u, 0, G);
   };
 
-  for (int pid = claim(); pid < args.B; pid = claim()) {
-  if (pid < args.B) {
+  // Lockstep (LOCK): the groups of a warp claim together, the iteration loop's
+  // trip count is the warp's (a group whose problem is done idles until the other
+  // finishes), and they claim again together. Free-running, a group that finishes claims
+  // at once; the groups then drift apart (one rolling out a new problem while the other is
+  // mid-iteration) and the warp issues each group's instructions separately. Measured
+  // (B=16384, T=10, 13/4 dense f32): free is 3% faster on the hover batch (iteration
+  // counts 3-4, lockstep idles a group for E[max]-E[it] = 0.3 iterations per pair);
+  // lockstep is 5% faster on random costs (2-10 iterations) and 21% faster at conv_tol=0
+  // (free: 14.8 active threads per warp instruction).
+  auto wany = [&](bool v) -> bool {
+    if constexpr (LOCK) return __any_sync(wm, v);
+    else return v;
+  };
+  for (int pid_ = claim(); wany(pid_ < args.B); pid_ = claim()) {
+  const bool live = !LOCK || pid_ < args.B;
+  const int pid = live ? pid_ : 0;  // a group past the end reads problem 0, writes nothing
+  {
   double* Un = Ubuf0;  // nominal controls (swapped with the alpha_0 candidate's on accept)
   double* Us = Ubuf1;
   const R* Cg = (const R*)args.C + (size_t)pid * T * D::NCS;
@@ -173,7 +189,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   // the initial rollout stages C_t / c_t element-wise from the caller's arrays and writes
   // them out as packed, 16-byte aligned records (Pw); every later sweep and line search
   // stages those with 16-byte copies
-  R* Pw = (R*)args.Pw + (size_t)pid * args.pw_stride;
+  R* Pw = (R*)args.Pw + (size_t)pid * args.pw_stride;  // (written only when live)
   CostPipe<M, DIAG, R, G> fwdp{&S, Cg, cg, T, lane, +1};
   CostPipe<M, DIAG, R, G> bwdp{&S, Cg, cg, T, lane, -1, nullptr, nullptr, Pw};
   CostPipe<M, DIAG, R, G> lsp{&S, Cg, cg, T, lane, +1, Kw, Kb, Pw};
@@ -286,13 +302,14 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   double J = 0.0;
   int active = 1, fail_t = -1, iterations = 0, converged = 0, diverged = 0;
   int k_lo = T;  // gains output rows [k_lo, T) were written by some sweep
-  R* ahist = args.alpha_hist ? (R*)args.alpha_hist + (size_t)pid * args.K_max : nullptr;
-  R* jhist = args.J_hist ? (R*)args.J_hist + (size_t)pid * (args.K_max + 1) : nullptr;
+  R* ahist = args.alpha_hist && live ? (R*)args.alpha_hist + (size_t)pid * args.K_max : nullptr;
+  R* jhist = args.J_hist && live ? (R*)args.J_hist + (size_t)pid * (args.K_max + 1) : nullptr;
+  if (!live) active = 0;
   if (ahist)
     for (int e = lane; e < args.K_max; e += G) ahist[e] = R(0);
 
   // =========================== initial rollout (kernels.py:161-178) ===========
-  {
+  if (live) {
     double xc[NX];
     lds_row_d<NX>(Xn, xc);
     fwdp.start(0);
@@ -332,8 +349,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   if (jhist && lane == 0) jhist[0] = (R)J;
 
   // =============================== iterations ==================================
-  int it = 0;
-  for (; it < args.K_max && active; it++) {
+  int it = 0, passes = 0;
+  for (; it < args.K_max && wany(active); it++) {
+    if constexpr (LOCK) {
+      if (!active) continue;  // done: wait for the warp's other groups
+      passes++;
+    }
     // ------------------- stage 1+2: fused linearise + Riccati sweep -------------
     R vxx[RPL][NX];  // the lane's rows of V_xx (value Hessian), carried across stages
 #pragma unroll
@@ -683,11 +704,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     if (jhist && lane == 0) jhist[it + 1] = (R)J;
   }
   if (jhist && lane == 0)
-    for (int e = it + 1; e <= args.K_max; e++) jhist[e] = (R)J;
+    for (int e = (LOCK ? passes : it) + 1; e <= args.K_max; e++) jhist[e] = (R)J;
 
   // ================================ outputs ====================================
   const bool failed = fail_t >= 0 || diverged;
-  {
+  if (live) {
     R* Xo = (R*)args.X + (size_t)pid * (T + 1) * NX;
     #pragma unroll 1
     for (int e = lane; e < (T + 1) * NX; e += G) Xo[e] = (R)Xn[(e / NX) * XLD + e % NX];
@@ -721,10 +742,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     }
   }
   __syncwarp(gm);
-  // the problem's gain / record lines are dead: drop them from L2 instead of writing back
-  for (int l = lane; l < (int)(args.kw_stride * sizeof(R) / 128); l += G) l2_discard((const char*)Kw + 128 * l);
-  for (int l = lane; l < (int)(args.pw_stride * sizeof(R) / 128); l += G) l2_discard((const char*)Pw + 128 * l);
-  }  // pid < B
+  // (The workspace lines of a finished problem are NOT dropped with discard.global.L2: doing
+  // so made ~100 of 16384 fixed-work solves differ run to run from their first iteration on,
+  // while the write-back it saves is ~240 MB per launch, <2% of HBM time.)
+  }  // problem scope
   }  // persistent loop
 }
 

@@ -63,8 +63,7 @@ int num_sms();
 // Forward workspace: [work counter (256 B)] [gains K (B, T, NU, LDA) of R]
 //                    [packed cost records (B, T, REC) of R]
 inline size_t rup128(size_t v) { return (v + 127) / 128 * 128; }
-// per-problem strides (bytes), 128-byte multiples so a finished problem's lines can be
-// discarded from L2 without touching a neighbour's
+// per-problem strides (bytes), 128-byte multiples: no L2 line is shared by two problems
 inline size_t fwd_gain_stride(int T, int nx, int nu, int elem) {
   const int vn = 16 / elem;
   const size_t lda = (size_t)((nx + vn - 1) / vn * vn);
@@ -125,7 +124,15 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
       return 0;
     }
   }
-  auto kern = ilqr_forward_kernel<M, G, DIAG, R>;
+  // warp lockstep of the groups (ilqr_forward_kernel): auto = fixed-work solves
+  // (conv_tol <= 0: every problem runs ~K_max iterations); DIFFMPC_LOCKSTEP=0|1 forces it
+  static int ls_env = -2;
+  if (ls_env == -2) {
+    const char* e = getenv("DIFFMPC_LOCKSTEP");
+    ls_env = e ? (atoi(e) != 0) : -1;
+  }
+  const bool lock = ls_env >= 0 ? ls_env != 0 : p->conv_tol <= 0.0;
+  auto kern = lock ? ilqr_forward_kernel<M, G, DIAG, R, true> : ilqr_forward_kernel<M, G, DIAG, R, false>;
   int per_sm = 1;
   if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)) return -1;
   if (const char* e = getenv("DIFFMPC_GPB")) {  // tuning override (even, keeps warps full)

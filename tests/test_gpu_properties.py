@@ -183,6 +183,48 @@ for i in range(30):
     subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=dict(os.environ, DIFFMPC_FWD="lat"))
 
 
+def test_lockstep_and_free_groups_agree_and_repeat():
+    """The throughput forward's two group schedules (warp lockstep / free-running, the
+    DIFFMPC_LOCKSTEP knob) give bit-identical results, repeatably, on batches with mixed
+    iteration counts and at conv_tol = 0 (a schedule-dependent stale read once showed up
+    exactly there: ~100 of 16384 fixed-work solves differing run to run)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2605_29155_b200 import DynModel, problems, solver
+m = DynModel.quadrotor()
+out = {}
+for name, pb in (("fixed", problems.hover_problem(m, 16384, 10, seed=0, conv_tol=0.0)),
+                 ("random", problems.random_problem(m, 4096, 10, seed=3))):
+    C = torch.tensor(pb.dense_C(), dtype=torch.float32, device="cuda")
+    args = [torch.tensor(a, dtype=torch.float32, device="cuda") for a in (pb.x0, pb.c, pb.U_warm)]
+    ref = None
+    for r in range(3):
+        o = solver.solve_raw(m, pb.settings, args[0], C, args[1], args[2], kernel="throughput")
+        if ref is None:
+            ref = o
+        else:
+            assert torch.equal(o.U, ref.U) and torch.equal(o.iters, ref.iters), (name, r)
+    out[name + "_U"] = ref.U.cpu().numpy()
+    out[name + "_it"] = ref.iters.cpu().numpy()
+np.savez(sys.argv[1], **out)
+'''
+    res = []
+    for ls in ("0", "1"):
+        f = os.path.join(tempfile.mkdtemp(), "o.npz")
+        subprocess.run([sys.executable, "-c", code, f], check=True, cwd=root,
+                       env=dict(os.environ, DIFFMPC_LOCKSTEP=ls))
+        res.append(np.load(f))
+    for k in res[0].files:
+        np.testing.assert_array_equal(res[0][k], res[1][k], err_msg=k)
+
+
 @pytest.mark.parametrize("layout", ["dense", "diag"])
 def test_solve_plan_matches_solve_raw(layout):
     """The preallocated launch path gives the same results as the allocating API."""

@@ -15,10 +15,13 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 only = os.environ.get("AB_ONLY", "")
 
 
-def run(name, model, B, T, dtype, layout):
+def run(name, model, B, T, dtype, layout, gen="hover", **kw):
     if only and only not in name:
         return
-    pb = problems.hover_problem(model, B, T, seed=0)
+    if gen == "hover":
+        pb = problems.hover_problem(model, B, T, seed=0, **kw)
+    else:
+        pb = problems.random_problem(model, B, T, **kw)
     dev = torch.device("cuda")
     C = torch.tensor(pb.diag if layout == "diag" else pb.dense_C(), device=dev, dtype=dtype)
     x0, c, Uw = (torch.tensor(a, device=dev, dtype=dtype) for a in (pb.x0, pb.c, pb.U_warm))
@@ -49,3 +52,5 @@ run("quad13-f32-diag", q, 16384, 10, torch.float32, "diag")
 run("quad13-f64-dense", q, 16384, 10, torch.float64, "dense")
 run("planar-f32-dense", p, 16384, 10, torch.float32, "dense")
 run("quad13-f32-dense-B256", q, 256, 10, torch.float32, "dense")
+run("quad13-f32-dense-random", q, 16384, 10, torch.float32, "dense", gen="random")
+run("quad13-f32-dense-fixed", q, 16384, 10, torch.float32, "dense", conv_tol=0.0)

@@ -9,7 +9,7 @@ import sys
 rep = sys.argv[1]
 kre = sys.argv[2] if len(sys.argv) > 2 else "ilqr_forward"
 obj = sys.argv[3] if len(sys.argv) > 3 else "paper_2605_29155_b200/build/inst_Quad13_float.o"
-fn = sys.argv[4] if len(sys.argv) > 4 else "_ZN4dmpc19ilqr_forward_kernelINS_6Quad13ELi16ELb0EfEEvNS_7FwdArgsE"
+fn = sys.argv[4] if len(sys.argv) > 4 else "_ZN4dmpc19ilqr_forward_kernelINS_6Quad13ELi16ELb0EfLb0EEEvNS_7FwdArgsE"
 out = subprocess.run([sys.executable, "tools/ncu_lines.py", rep, kre, obj, fn, "2000"], capture_output=True,
                      text=True).stdout
 src = open("paper_2605_29155_b200/csrc/ilqr_forward.cuh").read().splitlines()
