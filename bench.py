@@ -89,6 +89,11 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # wait for the first sample: nvidia-smi's NVML start-up on a fresh box can stall
+            # the GPU for tens of ms, which must not land inside a timed region
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
@@ -234,6 +239,7 @@ def run_ours(args):
     elapsed_ms = t_start.elapsed_time(t_end)
     fwd_ms = float(np.mean([a.elapsed_time(b) for a, b, _ in ev]))
     bwd_ms = float(np.mean([b.elapsed_time(c) for _, b, c in ev]))
+    step_max = float(max(a.elapsed_time(c) for a, _, c in ev))  # a stall inside the timed region shows here
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -376,7 +382,7 @@ def run_ours(args):
                 "gpu_launches": int(gpu_launches),
                 "launches_per_step": gpu_launches / args.steps,
                 "launches_per_ilqr_iteration": (gpu_launches / args.steps - 1) / float(iters.max().item()),
-                "forward_ms": fwd_ms, "backward_ms": bwd_ms,
+                "forward_ms": fwd_ms, "backward_ms": bwd_ms, "step_ms_max": step_max,
                 "mean_iters": float(iters.mean().item()), "max_iters": int(iters.max().item()),
                 "latency": lat,
                 "fixed_work": dict(fixed, roofline_frac=fixed["fwd_tflops"] / peak),
