@@ -45,6 +45,30 @@ DMPC_DEV void lds_row(const R* __restrict__ p, R (&v)[N]) {
   }
 }
 
+// Store a row to a 16-byte aligned, padded shared row with vector stores (pads get 0).
+template <int N, class R>
+DMPC_DEV void sts_row(R* __restrict__ p, const R (&v)[N]) {
+  if constexpr (sizeof(R) == 4) {
+#pragma unroll
+    for (int q = 0; q < (N + 3) / 4; q++) {
+      float4 t;
+      t.x = v[4 * q];
+      t.y = 4 * q + 1 < N ? v[4 * q + 1] : 0.f;
+      t.z = 4 * q + 2 < N ? v[4 * q + 2] : 0.f;
+      t.w = 4 * q + 3 < N ? v[4 * q + 3] : 0.f;
+      reinterpret_cast<float4*>(p)[q] = t;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < (N + 1) / 2; q++) {
+      double2 t;
+      t.x = v[2 * q];
+      t.y = 2 * q + 1 < N ? v[2 * q + 1] : 0.0;
+      reinterpret_cast<double2*>(p)[q] = t;
+    }
+  }
+}
+
 template <int N>
 DMPC_DEV void lds_row_d(const double* __restrict__ p, double (&v)[N]) {
 #pragma unroll
@@ -60,7 +84,12 @@ template <class M, bool DIAG, class R>
 struct Dims {
   static constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   static constexpr int VN = VecW<R>::N;
-  static constexpr int LDA = rup(NX, VN);  // rows of A, MA, Vx
+  static constexpr int LDA = rup(NX, VN);  // rows of A, Vx
+  // rows of MA: each lane writes (and reads back with vector loads) its own row, so an
+  // even number of 16-byte chunks per row (64 B at 13 f32) would put lanes a and a+2 on
+  // the same banks; an odd count (80 B) spreads the 8 lanes of a 128-bit phase over all
+  // 32 banks and leaves the scalar column stores 2-way instead of 8-way
+  static constexpr int LDM = (LDA / VN) % 2 == 0 ? LDA + VN : LDA;
   static constexpr int LDB = rup(NU, VN);  // rows of B, NB, K^T, Qux^T, (QuuK)^T, Quu
   static constexpr int ZLD = rup(NZ, VN);  // z, c, rows of staged dense C
   static constexpr int NCSP = DIAG ? ZLD : NZ * ZLD;  // staged C_t (padded rows)
@@ -82,7 +111,7 @@ struct RicLayout {
     auto take = [&](int n) { int r = o; o = rup(o + n * s, 16); return r; };
     L.oAs = take(D::NX * D::LDA);
     L.oBs = take(D::NX * D::LDB);
-    L.oMA = take(D::NX * D::LDA);
+    L.oMA = take(D::NX * D::LDM);
     L.oNB = take(D::NX * D::LDB);
     L.oKT = take(D::NX * D::LDB);
     L.oQuu = take(D::NU * D::LDB);
@@ -335,10 +364,8 @@ DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][
   for (int k = 0; k < RPL; k++) {
     const int a = row_of<G, RPL>(lane, k);
     if (a < NX) {
-#pragma unroll
-      for (int b = 0; b < NX; b++) S.MA[a * D::LDA + b] = ma[k][b];
-#pragma unroll
-      for (int b = 0; b < NU; b++) S.NB[a * D::LDB + b] = nb[k][b];
+      sts_row<NX>(S.MA + a * D::LDM, ma[k]);
+      sts_row<NU>(S.NB + a * D::LDB, nb[k]);
     }
   }
 }
@@ -375,7 +402,7 @@ DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&q
     rows.get(r, arow, brow);
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
-      const R mra = S.MA[r * D::LDA + ac[k]];
+      const R mra = S.MA[r * D::LDM + ac[k]];
 #pragma unroll
       for (int bb = 0; bb < NX; bb++) {
         if (M::a_one(r, bb)) qxx[k][bb] += mra;
@@ -447,7 +474,7 @@ DMPC_DEV void ric_Vxx_rows(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RP
           s0 += quxc[k][r] * kk[r];
           if (r + 1 < NU) s1 += quxc[k][r + 1] * kk[r + 1];
         }
-        if (a < NX) S.MA[a * D::LDA + bb] = s0 + s1;
+        if (a < NX) S.MA[a * D::LDM + bb] = s0 + s1;
       }
     }
     return;
@@ -470,7 +497,7 @@ DMPC_DEV void ric_Vxx_rows(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RP
       R s = qxx[k][bb];
 #pragma unroll
       for (int r = 0; r < NU; r++) s += (kcol[k][r] * kq[r] + kcol[k][r] * qx[r]) + quxc[k][r] * kk[r];
-      if (a < NX) S.MA[a * D::LDA + bb] = s;
+      if (a < NX) S.MA[a * D::LDM + bb] = s;
     }
   }
 }
@@ -485,9 +512,9 @@ DMPC_DEV void ric_symmetrize(const Ric<M, DIAG, R>& S, int lane, R (&vxx)[RPL][M
     const int a = row_of<G, RPL>(lane, k);
     if (a < NX) {
       R row[NX];
-      lds_row<NX>(S.MA + a * D::LDA, row);
+      lds_row<NX>(S.MA + a * D::LDM, row);
 #pragma unroll
-      for (int bb = 0; bb < NX; bb++) vxx[k][bb] = R(0.5) * (row[bb] + S.MA[bb * D::LDA + a]);
+      for (int bb = 0; bb < NX; bb++) vxx[k][bb] = R(0.5) * (row[bb] + S.MA[bb * D::LDM + a]);
     } else {
 #pragma unroll
       for (int bb = 0; bb < NX; bb++) vxx[k][bb] = R(0);
