@@ -34,7 +34,10 @@ int check_theta(const DiffMPCProblem* p) {
 template <class Lay, class K>
 int plan(K kern, int B, int T, int G, int& gpb, int& stride, int* per_sm = nullptr) {
   const Lay L = Lay::make(T);
-  stride = L.total;
+  // per-group stride = whole 128-byte lines + G banks: the 32/G groups of a warp start G
+  // banks apart, so a warp-wide access of consecutive elements (lane = row or column
+  // index, one per group) covers all 32 banks instead of hitting the same 16 twice
+  stride = (L.total + 127) / 128 * 128 + 4 * G;
   const int limit = max_smem_optin();
   int best = -1, best_res = -1;
   for (int g = 128 / G; g >= 1; g /= 2) {

@@ -439,11 +439,9 @@ DMPC_DEV void ric_publish_cols(const Ric<M, DIAG, R>& S, int a, const R (&kcol)[
                                bool lean) {
   using D = Dims<M, DIAG, R>;
   constexpr int NU = M::NU;
-#pragma unroll
-  for (int i = 0; i < NU; i++) S.KT[a * D::LDB + i] = kcol[i];
+  sts_row<NU>(S.KT + a * D::LDB, kcol);  // one vector store per lane: no bank conflicts
   if (lean) return;
-#pragma unroll
-  for (int i = 0; i < NU; i++) S.QuxT[a * D::LDB + i] = quxc[i];
+  sts_row<NU>(S.QuxT + a * D::LDB, quxc);
 }
 
 // newVxx rows -> N (aliases MA) (kernels.py:499-507):
@@ -460,6 +458,9 @@ DMPC_DEV void ric_Vxx_rows(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RP
                            const R (&quu)[M::NU][M::NU], bool lean) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU;
+  // each lane's row is assembled in registers and stored with vector stores (a column of
+  // scalar stores, one per lane-owned row, is bank-conflicted)
+  R vrow[RPL][NX];
   if (lean) {
 #pragma unroll
     for (int bb = 0; bb < NX; bb++) {
@@ -467,15 +468,19 @@ DMPC_DEV void ric_Vxx_rows(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RP
       lds_row<NU>(S.KT + bb * D::LDB, kk);
 #pragma unroll
       for (int k = 0; k < RPL; k++) {
-        const int a = row_of<G, RPL>(lane, k);
         R s0 = qxx[k][bb], s1 = R(0);
 #pragma unroll
         for (int r = 0; r < NU; r += 2) {
           s0 += quxc[k][r] * kk[r];
           if (r + 1 < NU) s1 += quxc[k][r + 1] * kk[r + 1];
         }
-        if (a < NX) S.MA[a * D::LDM + bb] = s0 + s1;
+        vrow[k][bb] = s0 + s1;
       }
+    }
+#pragma unroll
+    for (int k = 0; k < RPL; k++) {
+      const int a = row_of<G, RPL>(lane, k);
+      if (a < NX) sts_row<NX>(S.MA + a * D::LDM, vrow[k]);
     }
     return;
   }
@@ -493,12 +498,16 @@ DMPC_DEV void ric_Vxx_rows(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RP
     }
 #pragma unroll
     for (int k = 0; k < RPL; k++) {
-      const int a = row_of<G, RPL>(lane, k);
       R s = qxx[k][bb];
 #pragma unroll
       for (int r = 0; r < NU; r++) s += (kcol[k][r] * kq[r] + kcol[k][r] * qx[r]) + quxc[k][r] * kk[r];
-      if (a < NX) S.MA[a * D::LDM + bb] = s;
+      vrow[k][bb] = s;
     }
+  }
+#pragma unroll
+  for (int k = 0; k < RPL; k++) {
+    const int a = row_of<G, RPL>(lane, k);
+    if (a < NX) sts_row<NX>(S.MA + a * D::LDM, vrow[k]);
   }
 }
 
