@@ -118,10 +118,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   }
   const R dt_r = (R)args.dt;
   if constexpr (M::kLinearParams) {
-    for (int e = lane; e < NX * NX; e += G) S.As[(e / NX) * LDA + e % NX] = thg[e];
+    for (int e = lane; e < NX * NX; e += G) S.As[(e / NX) * D::LDM + e % NX] = thg[e];
     for (int e = lane; e < NX * NU; e += G) S.Bs[(e / NU) * LDB + e % NU] = thg[NX * NX + e];
   } else {
-    M::template jac_const<R>(P_r, dt_r, S.As, LDA, S.Bs, LDB, lane, G);
+    M::template jac_const<R>(P_r, dt_r, S.As, D::LDM, S.Bs, LDB, lane, G);
   }
   {
     const R* xg = (const R*)args.X + (size_t)pid * (T + 1) * NX;
@@ -172,9 +172,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       using Rows = std::conditional_t<has_jac_regs<M>::value, RegRows<M, R>, SmemRows<M, DIAG, R>>;
       Rows rows = make_rows<M, DIAG, R>(S, P_r, dt_r, zr);
       if constexpr (has_jac_regs<M>::value) {
-        jac_store_rows<M, R>(rows, S.As, LDA, S.Bs, LDB);
+        jac_store_rows<M, R>(rows, S.As, D::LDM, S.Bs, LDB);
       } else if constexpr (!M::kLinearParams) {
-        M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
+        M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, D::LDM, S.Bs, LDB);
       }
       __syncwarp(gm);
       R qx[RPL];
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         const int a = min(row_of<G, RPL>(lane, k), NX - 1);
         R s = dXs[t * LDA + a];
 #pragma unroll
-        for (int b2 = 0; b2 < NX; b2++) s += S.As[b2 * LDA + a] * vx[b2];
+        for (int b2 = 0; b2 < NX; b2++) s += S.As[b2 * D::LDM + a] * vx[b2];
         qx[k] = s;
       }
       for (int a = lane; a < NU; a += G) {
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       R xr[NX], ur[NU];
       lds_row<NX>(Xs + t * LDA, xr);
       lds_row<NU>(Us + t * LDB, ur);
-      if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
+      if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, D::LDM, S.Bs, LDB);
       R dx[NX];
       lds_row<NX>(dXs + t * LDA, dx);
       for (int r = lane; r < NU; r += G) {
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         const int a = row_of<G, RPL>(lane, k);
         if (a < NX) {
           R arow[NX], brow[NU];
-          lds_row<NX>(S.As + a * LDA, arow);
+          lds_row<NX>(S.As + a * D::LDM, arow);
           lds_row<NU>(S.Bs + a * LDB, brow);
           R s = R(0);
 #pragma unroll
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         lds_row<NX>(lams, lm);
         lds_row<NX>(lhs, lh);
         __syncwarp(gm);
-        if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
+        if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, D::LDM, S.Bs, LDB);
         __syncwarp(gm);
         if (want_theta) {
           if constexpr (M::kLinearParams) {
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           }
 #pragma unroll
           for (int b = 0; b < NX; b++) {
-            const R ab = S.As[b * LDA + a];
+            const R ab = S.As[b * D::LDM + a];
             s1 += ab * lm[b];
             s2 += ab * lh[b];
           }

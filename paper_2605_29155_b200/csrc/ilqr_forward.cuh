@@ -83,7 +83,7 @@ struct FwdLayout {
     L.oUs = o; o += T * D::ULD * 8;
     L.okg = o; o += T * D::ULD * 8;
     o = align_up(o, 16);
-    L.oKb = o; o += D::NBUF * D::NU * D::LDA * (int)sizeof(R);
+    L.oKb = o; o += D::NBUF * D::NU * D::LDM * (int)sizeof(R);
     o = align_up(o, 16);
     L.ric = RicLayout<M, DIAG, R>::make(o);
     L.total = align_up(L.ric.end, 16);
@@ -222,10 +222,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
 
   // ---- constant Jacobian structure (written once) ----
   if constexpr (M::kLinearParams) {
-    for (int e = lane; e < NX * NX; e += G) S.As[(e / NX) * LDA + e % NX] = thg[e];
+    for (int e = lane; e < NX * NX; e += G) S.As[(e / NX) * D::LDM + e % NX] = thg[e];
     for (int e = lane; e < NX * NU; e += G) S.Bs[(e / NU) * LDB + e % NU] = thg[NX * NX + e];
   } else {
-    M::template jac_const<R>(P_r, dt_r, S.As, LDA, S.Bs, LDB, lane, G);
+    M::template jac_const<R>(P_r, dt_r, S.As, D::LDM, S.Bs, LDB, lane, G);
   }
 
   // ---- load x0, U_warm (clipped, ilqr.py:165); zero K, k (Workspace init) ----
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       __syncwarp(gm);
       fwdp.release(t);
       double xn[NX];
-      step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
+      step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xc, u, xn);
       bool fin = true;
 #pragma unroll
       for (int i = 0; i < NX; i++) {
@@ -380,14 +380,14 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       using Rows = std::conditional_t<has_jac_regs<M>::value, RegRows<M, R>, SmemRows<M, DIAG, R>>;
       Rows rows = make_rows<M, DIAG, R>(S, P_r, dt_r, zv);
       if constexpr (has_jac_regs<M>::value) {
-        jac_store_rows<M, R>(rows, S.As, LDA, S.Bs, LDB);
+        jac_store_rows<M, R>(rows, S.As, D::LDM, S.Bs, LDB);
       } else if constexpr (!M::kLinearParams) {
         R xr[NX], ur[NU];
 #pragma unroll
         for (int i = 0; i < NX; i++) xr[i] = zv[i];
 #pragma unroll
         for (int i = 0; i < NU; i++) ur[i] = zv[NX + i];
-        M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, LDA, S.Bs, LDB);
+        M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, D::LDM, S.Bs, LDB);
       }
       __syncwarp(gm);
       // gz = C z + c ; qx = gz_x + A' Vx ; qu = gz_u + B' Vx   (kernels.py:395-410)
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           for (int b2 = 0; b2 < NZ; b2++) sa[b2 & 1] += crow[b2] * zv[b2];
         }
 #pragma unroll
-        for (int b2 = 0; b2 < NX; b2++) sa[2 + (b2 & 1)] += S.As[b2 * LDA + a] * vx[b2];
+        for (int b2 = 0; b2 < NX; b2++) sa[2 + (b2 & 1)] += S.As[b2 * D::LDM + a] * vx[b2];
         qx[k] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
       }
       for (int a = lane; a < NU; a += G) {
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
             if (r < NU) {
               v = Un[t * ULD + r] + alpha * kg[t * ULD + r];
               R krow[NX];
-              lds_row<NX>(lsp.K(t) + r * LDA, krow);
+              lds_row<NX>(lsp.K(t) + r * D::LDM, krow);
               v = feedback<NX>(v, krow, xc, xbar);
               const double lo = args.u_min[r], hi = args.u_max[r];
               if (v < lo) v = lo;
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           }
           lsp.release(t);
           double xn[NX];
-          step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xc, u, xn);
+          step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xc, u, xn);
           bool fin = true;
 #pragma unroll
           for (int i = 0; i < NX; i++) {
@@ -674,11 +674,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
             if (lane + m2 * G < NU) Un[t * ULD + lane + m2 * G] = v[m2];
         }
         double xn[NX];
-        step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xb, ub, xn);
+        step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xb, ub, xn);
 #pragma unroll
         for (int i = 0; i < NX; i++) xb[i] = xn[i];
         if (accept) {
-          step_e<M, R>(P_e, dt_e, S.As, LDA, S.Bs, LDB, xw, uw, xn);
+          step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xw, uw, xn);
 #pragma unroll
           for (int i = 0; i < NX; i++) xw[i] = xn[i];
         }

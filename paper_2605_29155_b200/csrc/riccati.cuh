@@ -109,7 +109,7 @@ struct RicLayout {
     RicLayout L;
     const int s = (int)sizeof(R);
     auto take = [&](int n) { int r = o; o = rup(o + n * s, 16); return r; };
-    L.oAs = take(D::NX * D::LDA);
+    L.oAs = take(D::NX * D::LDM);
     L.oBs = take(D::NX * D::LDB);
     L.oMA = take(D::NX * D::LDM);
     L.oNB = take(D::NX * D::LDB);
@@ -192,7 +192,7 @@ struct CostPipe {
   const R* cg;
   int T, lane, step;
   const R* Kg = nullptr;  // gain workspace of this problem, [t][NU][LDA]
-  R* Kb = nullptr;        // NBUF smem buffers of NU*LDA
+  R* Kb = nullptr;        // NBUF smem buffers of NU rows of LDM
   const R* Pk = nullptr;  // packed stage records [C_t padded rows | c_t padded] (REC elements)
   static constexpr int REC = D::REC;
   static constexpr int NCH = REC * (int)sizeof(R) / 16;  // 16-byte chunks per record
@@ -207,12 +207,16 @@ struct CostPipe {
     } else {
       stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, t, buf(t), lane);
     }
-    if (Kg) {
-      const char* src = (const char*)(Kg + (size_t)t * D::NU * D::LDA) + 16 * lane;
-      char* dst = (char*)(Kb + buf(t) * D::NU * D::LDA) + 16 * lane;
+    if (Kg) {  // rows of LDA in the workspace -> rows of LDM here (the line search reads
+               // four different K rows per 8-lane phase: 64-byte rows would collide)
+      constexpr int CPR = D::LDA * (int)sizeof(R) / 16;  // 16-byte chunks per row
+      const char* src = (const char*)(Kg + (size_t)t * D::NU * D::LDA);
+      char* dst = (char*)(Kb + buf(t) * D::NU * D::LDM);
 #pragma unroll
-      for (int k = 0; k < (KCH + G - 1) / G; k++)
-        if (k * G + lane < KCH) cp_async_16cg(dst + 16 * G * k, src + 16 * G * k);
+      for (int k = 0; k < (KCH + G - 1) / G; k++) {
+        const int c = k * G + lane;
+        if (c < KCH) cp_async_16cg(dst + (c / CPR) * D::LDM * (int)sizeof(R) + 16 * (c % CPR), src + 16 * c);
+      }
     }
     cp_async_commit();
   }
@@ -241,7 +245,7 @@ struct CostPipe {
   }
   DMPC_DEV const R* C(int t) const { return S->Cb(buf(t)); }
   DMPC_DEV const R* c(int t) const { return S->cb(buf(t)); }
-  DMPC_DEV const R* K(int t) const { return Kb + buf(t) * D::NU * D::LDA; }
+  DMPC_DEV const R* K(int t) const { return Kb + buf(t) * D::NU * D::LDM; }  // rows of LDM
 };
 
 // ---------------------------------------------------------------------------
@@ -281,7 +285,7 @@ struct SmemRows {
   const Ric<M, DIAG, R>& S;
   DMPC_DEV void get(int r, R (&a)[M::NX], R (&b)[M::NU]) const {
     using D = Dims<M, DIAG, R>;
-    if (a_row_sd<M>(r)) lds_row<M::NX>(S.As + r * D::LDA, a);
+    if (a_row_sd<M>(r)) lds_row<M::NX>(S.As + r * D::LDM, a);
     if (b_row_nz<M>(r)) lds_row<M::NU>(S.Bs + r * D::LDB, b);
   }
   DMPC_DEV R b(int r, int i) const { return S.Bs[r * Dims<M, DIAG, R>::LDB + i]; }  // B[r][i]
