@@ -65,7 +65,7 @@ struct BwdLayout {
 };
 
 template <class M, int G, bool DIAG, class R>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : 3)) : 2) ilqr_backward_kernel(const BwdArgs args) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 || DIAG ? 4 : 3)) : 2) ilqr_backward_kernel(const BwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD;
