@@ -128,7 +128,7 @@ DMPC_DEV double feedback(double v, const R (&krow)[NX], const double (&x)[NX], c
 }
 
 template <class M, int G, bool DIAG, class R, bool LOCK>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (DIAG || M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD, XLD = D::XLD, ULD = D::ULD;
