@@ -37,6 +37,9 @@ def main():
                          "PPO iterations (batched race env rollout collection + update, planar model)")
     ap.add_argument("--envs", type=int, default=1024, help="train mode: environments per GPU")
     ap.add_argument("--rollout-steps", type=int, default=32, help="train mode: steps per update")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="update mode: eager minibatch steps (default: one CUDA graph per step when "
+                         "no gradient collective runs, i.e. one process)")
     args = ap.parse_args()
     if args.mode == "train":
         return train_mode(args)
@@ -82,8 +85,17 @@ def main():
              "advantages": torch.randn(B, device=dev, generator=g), "returns": torch.randn(B, device=dev, generator=g),
              "x_init": x_init, "U_warm": U_warm}
     sink = {}
+    use_graph = world == 1 and not args.no_graph
+    if use_graph:
+        gstep = ppo.GraphedMinibatchStep(bundle, opt, batch, cfg, solver)
+
+        def step(sink_):
+            gstep(batch)
+    else:
+        def step(sink_):
+            ppo.minibatch_step(bundle, opt, batch, cfg, solver, reducer, sink_)
     for _ in range(args.warmup):
-        ppo.minibatch_step(bundle, opt, batch, cfg, solver, reducer, sink)
+        step(sink)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -92,7 +104,7 @@ def main():
     sink = {}
     a.record()
     for _ in range(args.steps):
-        ppo.minibatch_step(bundle, opt, batch, cfg, solver, reducer, sink)
+        step(sink)
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / args.steps
@@ -100,7 +112,7 @@ def main():
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    launches = (_lib.launch_count() - l0) / args.steps
+    launches = gstep.diffmpc_launches if use_graph else (_lib.launch_count() - l0) / args.steps
     if rank == 0:
         print(json.dumps({
             "metric": "AC-MPC PPO minibatch steps/s (DiffMPC actor fwd+bwd + NCCL grad all-reduce)",
@@ -111,7 +123,8 @@ def main():
                        "global_minibatch": B * world, "params": sum(p.numel() for p in bundle.parameters()),
                        "allreduce_bytes": reducer.nbytes, "parallelism": f"dp{world}"},
             "diffmpc_launches_per_step": launches,
-            "mean_solver_iters": float(sink.get("iterations", 0)) / max(1, sink.get("solves", 1)),
+            "cuda_graph": use_graph,
+            "mean_solver_iters": (float(sink.get("iterations", 0)) / max(1, sink.get("solves", 1))) if sink else None,
         }), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -90,7 +90,9 @@ def ppo_losses(bundle, batch, config: TrainConfig, solver=None, stats_sink=None)
     else:
         u_mean = bundle.actor(obs)
     sigma = torch.exp(bundle.log_sigma)
-    dist_ = torch.distributions.Normal(u_mean, sigma)
+    # no argument validation: it costs a host sync per call (and breaks graph capture); a
+    # non-finite mean or sigma gives a non-finite loss, i.e. the skipped minibatch
+    dist_ = torch.distributions.Normal(u_mean, sigma, validate_args=False)
     log_probs = dist_.log_prob(batch["actions"]).sum(-1)
     ratio = torch.exp(log_probs - batch["old_log_probs"])
     adv = batch["advantages"]
@@ -168,6 +170,57 @@ def minibatch_step(bundle, optimizer, batch, config: TrainConfig, solver=None, r
     torch.nn.utils.clip_grad_norm_([p for p in bundle.parameters() if p.grad is not None], config.grad_clip)
     optimizer.step()
     return loss.detach(), metrics
+
+
+class GraphedMinibatchStep:
+    """minibatch_step with the losses, the backward through the DiffMPC layer and the gradient
+    clipping replayed from one CUDA graph (single process, or whenever no collective runs).
+
+    The eager step issues ~130 kernel launches from Python (MLPs, distributions, the solver's
+    output allocations, autograd); replaying them as one graph leaves the GPU time. Each call
+    copies the minibatch into static buffers, replays the graph, reads the finite-loss flag
+    (the reference's skipped minibatch, trainer.py:200-212) and, if finite, runs the
+    optimizer step eagerly — the same arithmetic as ``minibatch_step`` on the same batch.
+    Warm-up passes (before capture) compute gradients only; parameters are untouched.
+    """
+
+    def __init__(self, bundle, optimizer, example_batch: dict, config: TrainConfig, solver=None, warmup: int = 3):
+        self.bundle, self.optimizer, self.config, self.solver = bundle, optimizer, config, solver
+        self.params = [p for p in bundle.parameters() if p.requires_grad]
+        self.static = {k: v.detach().clone() for k, v in example_batch.items()}
+        for p in self.params:
+            if p.grad is None:
+                p.grad = torch.zeros_like(p)
+        side = torch.cuda.Stream(device=self.params[0].device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self._body()
+        torch.cuda.current_stream().wait_stream(side)
+        from . import _lib
+        l0 = _lib.launch_count()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss, self.finite = self._body()
+        self.diffmpc_launches = _lib.launch_count() - l0  # DiffMPC kernels inside the graph
+
+    def _body(self):
+        for p in self.params:
+            p.grad.zero_()
+        loss, _ = ppo_losses(self.bundle, self.static, self.config, self.solver)
+        finite = torch.isfinite(loss.detach())
+        loss.backward()
+        torch.nn.utils.clip_grad_norm_(self.params, self.config.grad_clip)
+        return loss.detach(), finite
+
+    def __call__(self, batch: dict):
+        for k, v in batch.items():
+            self.static[k].copy_(v, non_blocking=True)
+        self.graph.replay()
+        if not bool(self.finite.item()):
+            return None
+        self.optimizer.step()
+        return self.loss
 
 
 def ppo_update(buffer: dict, bundle, optimizer, config: TrainConfig, solver=None, generator=None,

@@ -73,7 +73,7 @@ class DeviceRollout:
             values = b.critic(self.obs).to(torch.float64)
             eps = torch.randn(u_mean.shape, generator=self.gen, **f32)
             actions = u_mean + sigma * eps
-            log_probs = torch.distributions.Normal(u_mean, sigma).log_prob(actions).sum(-1)
+            log_probs = torch.distributions.Normal(u_mean, sigma, validate_args=False).log_prob(actions).sum(-1)
             u_exec = torch.clamp(actions.to(torch.float64), self.u_lo, self.u_hi)
             buf["obs"][s] = self.obs
             buf["actions"][s] = actions

@@ -45,9 +45,17 @@ def _as(t, dtype, device, shape=None, name="array"):
     return t
 
 
+_THETA_CACHE = {}
+
+
 def _theta(model, theta, dtype, device, B):
-    th = model.params if theta is None else theta
-    th = _as(th, dtype, device)
+    if theta is None:  # the model's own parameters: one device copy per (values, dtype, device)
+        key = (np.asarray(model.params, dtype=np.float64).tobytes(), dtype, str(device))
+        th = _THETA_CACHE.get(key)
+        if th is None:
+            th = _THETA_CACHE[key] = _as(model.params, dtype, device)
+    else:
+        th = _as(theta, dtype, device)
     if th.ndim == 1:
         if th.shape[0] != model.n_theta:
             raise ConfigError(f"theta must have {model.n_theta} entries, got {th.shape[0]}")

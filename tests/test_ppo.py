@@ -180,3 +180,50 @@ def test_device_rollout_collect_and_update():
     out = ppo.ppo_update(flat, b, opt, cfg, solver, generator=torch.Generator().manual_seed(0))
     assert out["skipped_minibatches"] == 0
     assert int(stats["solves"]) == 6 * 128
+
+
+@pytest.mark.gpu
+def test_graphed_minibatch_step_matches_eager():
+    """ppo.GraphedMinibatchStep (losses + backward through the DiffMPC layer + clipping
+    replayed from one CUDA graph, optimizer step eager) updates the parameters exactly like
+    the eager minibatch_step on the same batches."""
+    import copy
+
+    from paper_2605_29155_b200 import DynModel, ppo, problems
+    from paper_2605_29155_b200.layer import MpcSolver, mpc_control
+    from paper_2605_29155_b200.policy import CostHeadScaling, PolicyBundle
+
+    dev = torch.device("cuda")
+    model = DynModel.quadrotor(dt=0.05)
+    B, T = 256, 10
+    pb = problems.hover_problem(model, B, T, seed=3)
+    torch.manual_seed(0)
+    b1 = PolicyBundle("ac_mpc", 13, model, pb.settings, CostHeadScaling.for_model(model, 13)).to(dev)
+    b2 = copy.deepcopy(b1)
+    solver = MpcSolver(model, pb.settings, device=dev)
+    cfg = ppo.TrainConfig()
+    o1 = torch.optim.Adam(b1.parameters(), lr=cfg.lr_start)
+    o2 = torch.optim.Adam(b2.parameters(), lr=cfg.lr_start)
+    x_init = torch.tensor(pb.x0, dtype=torch.float32, device=dev)
+    U_warm = torch.tensor(pb.U_warm, dtype=torch.float32, device=dev)
+    g = torch.Generator(device=dev).manual_seed(5)
+
+    def make_batch():
+        with torch.no_grad():
+            u = mpc_control(b1, x_init, solver, x_init, U_warm)
+            sig = torch.exp(b1.log_sigma)
+            a = u + sig * torch.randn(u.shape, device=dev, generator=g)
+            lp = torch.distributions.Normal(u, sig).log_prob(a).sum(-1)
+        return {"obs": x_init.clone(), "actions": a, "old_log_probs": lp,
+                "advantages": torch.randn(B, device=dev, generator=g),
+                "returns": torch.randn(B, device=dev, generator=g), "x_init": x_init, "U_warm": U_warm}
+
+    batches = [make_batch() for _ in range(4)]
+    gstep = ppo.GraphedMinibatchStep(b2, o2, batches[0], cfg, solver)
+    assert gstep.diffmpc_launches == 2
+    for bt in batches:
+        l1, _ = ppo.minibatch_step(b1, o1, bt, cfg, solver)
+        l2 = gstep(bt)
+        torch.testing.assert_close(l2, l1, rtol=1e-5, atol=1e-6)
+    for p1, p2 in zip(b1.parameters(), b2.parameters()):
+        torch.testing.assert_close(p2, p1, rtol=1e-5, atol=1e-6)
