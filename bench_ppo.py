@@ -165,9 +165,18 @@ def train_mode(args):
     col = DeviceRollout(bundle, solver, env, cfg, seed=5 + rank)
     gen = torch.Generator().manual_seed(3)
 
+    graphed = []
+
     def iteration():
         flat, stats = col.collect()
-        m = ppo.ppo_update(flat, bundle, opt, cfg, solver, generator=gen, reducer=reducer, rank=rank, world=world)
+        if not graphed and world == 1 and not args.no_graph:
+            mb = min(cfg.minibatch_size, flat["obs"].shape[0])
+            ex = {"obs": flat["obs"][:mb], "actions": flat["actions"][:mb], "old_log_probs": flat["log_probs"][:mb],
+                  "advantages": flat["advantages"][:mb].float(), "returns": flat["returns"][:mb].float(),
+                  "x_init": flat["x_init"][:mb], "U_warm": flat["U_warm"][:mb]}
+            graphed.append(ppo.GraphedMinibatchStep(bundle, opt, ex, cfg, solver))
+        m = ppo.ppo_update(flat, bundle, opt, cfg, solver, generator=gen, reducer=reducer, rank=rank, world=world,
+                           graphed=graphed[0] if graphed else None)
         return stats, m
 
     for _ in range(max(1, args.warmup // 3)):
@@ -200,6 +209,7 @@ def train_mode(args):
                        "rollout_steps": args.rollout_steps, "minibatch_per_gpu": args.minibatch // world,
                        "parallelism": f"dp{world}"},
             "diffmpc_launches_per_iteration": (_lib.launch_count() - l0) / K,
+            "update_cuda_graph": bool(graphed),
             "mean_solver_iters": float(stats["solver_iters"]) / stats["solves"],
             "episodes_last_iteration": int(stats["episodes"]),
         }), flush=True)

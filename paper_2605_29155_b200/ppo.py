@@ -207,16 +207,25 @@ class GraphedMinibatchStep:
     def _body(self):
         for p in self.params:
             p.grad.zero_()
-        loss, _ = ppo_losses(self.bundle, self.static, self.config, self.solver)
+        self.sink = {}  # per-replay solver counters (the tensors written by the graph)
+        loss, self.metrics = ppo_losses(self.bundle, self.static, self.config, self.solver, self.sink)
         finite = torch.isfinite(loss.detach())
         loss.backward()
         torch.nn.utils.clip_grad_norm_(self.params, self.config.grad_clip)
         return loss.detach(), finite
 
-    def __call__(self, batch: dict):
+    def matches(self, batch: dict) -> bool:
+        return all(k in self.static and self.static[k].shape == v.shape for k, v in batch.items())
+
+    def __call__(self, batch: dict, stats_sink=None):
+        """One step; returns the loss (a static tensor, valid until the next call) or None for
+        a skipped minibatch. ``self.metrics`` holds this step's metrics (static tensors)."""
         for k, v in batch.items():
             self.static[k].copy_(v, non_blocking=True)
         self.graph.replay()
+        if stats_sink is not None:
+            for k, v in self.sink.items():
+                stats_sink[k] = stats_sink.get(k, 0) + v
         if not bool(self.finite.item()):
             return None
         self.optimizer.step()
@@ -224,12 +233,14 @@ class GraphedMinibatchStep:
 
 
 def ppo_update(buffer: dict, bundle, optimizer, config: TrainConfig, solver=None, generator=None,
-               reducer=None, rank: int = 0, world: int = 1):
+               reducer=None, rank: int = 0, world: int = 1, graphed: GraphedMinibatchStep | None = None):
     """Epochs of shuffled-minibatch updates over a filled buffer (trainer.py:164-215).
 
     buffer: flat (n, ...) device tensors obs, actions, log_probs, advantages, returns
     (+ x_init, U_warm). Each rank processes its contiguous 1/world slice of every
     minibatch (the permutation is drawn from the shared generator, so all ranks agree).
+    ``graphed``: a GraphedMinibatchStep of this bundle/optimizer (one process) replaces the
+    eager step for every minibatch of its shape.
     """
     from .shard import shard_range
 
@@ -251,7 +262,11 @@ def ppo_update(buffer: dict, bundle, optimizer, config: TrainConfig, solver=None
             lo, hi = shard_range(sel.shape[0], rank, world)
             sel = sel[lo:hi]
             batch = {k: v[sel] for k, v in flat.items()}
-            loss, metrics = minibatch_step(bundle, optimizer, batch, config, solver, reducer, stats_sink)
+            if graphed is not None and graphed.matches(batch):
+                loss = graphed(batch, stats_sink)
+                metrics = {k: v.clone() for k, v in graphed.metrics.items()}
+            else:
+                loss, metrics = minibatch_step(bundle, optimizer, batch, config, solver, reducer, stats_sink)
             if loss is None:
                 skipped += 1
                 continue

@@ -227,3 +227,43 @@ def test_graphed_minibatch_step_matches_eager():
         torch.testing.assert_close(l2, l1, rtol=1e-5, atol=1e-6)
     for p1, p2 in zip(b1.parameters(), b2.parameters()):
         torch.testing.assert_close(p2, p1, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_ppo_update_with_graphed_step_matches_eager():
+    """ppo_update with a GraphedMinibatchStep gives the same parameters and statistics as the
+    eager update over the same buffer (same permutation generator)."""
+    import copy
+
+    from paper_2605_29155_b200 import DynModel, ppo, problems
+
+    dev = torch.device("cuda")
+    model = DynModel.quadrotor(dt=0.05)
+    n, T = 512, 10
+    pb = problems.hover_problem(model, n, T, seed=4)
+    torch.manual_seed(0)
+    from paper_2605_29155_b200.layer import MpcSolver
+    b1 = PolicyBundle("ac_mpc", 13, model, pb.settings, CostHeadScaling.for_model(model, 13)).to(dev)
+    b2 = copy.deepcopy(b1)
+    solver = MpcSolver(model, pb.settings, device=dev)
+    cfg = ppo.TrainConfig(minibatch_size=128, sgd_epochs=2)
+    o1 = torch.optim.Adam(b1.parameters(), lr=cfg.lr_start)
+    o2 = torch.optim.Adam(b2.parameters(), lr=cfg.lr_start)
+    g = torch.Generator(device=dev).manual_seed(9)
+    x = torch.tensor(pb.x0, dtype=torch.float32, device=dev)
+    buf = {"obs": x, "actions": torch.randn((n, 4), device=dev, generator=g),
+           "log_probs": torch.randn(n, device=dev, generator=g) - 3.0,
+           "advantages": torch.randn(n, device=dev, generator=g, dtype=torch.float64),
+           "returns": torch.randn(n, device=dev, generator=g, dtype=torch.float64),
+           "x_init": x, "U_warm": torch.tensor(pb.U_warm, dtype=torch.float32, device=dev)}
+    m1 = ppo.ppo_update(buf, b1, o1, cfg, solver, generator=torch.Generator().manual_seed(2))
+    ex = {"obs": x[:128], "actions": buf["actions"][:128], "old_log_probs": buf["log_probs"][:128],
+          "advantages": buf["advantages"][:128].float(), "returns": buf["returns"][:128].float(),
+          "x_init": x[:128], "U_warm": buf["U_warm"][:128]}
+    gs = ppo.GraphedMinibatchStep(b2, o2, ex, cfg, solver)
+    m2 = ppo.ppo_update(buf, b2, o2, cfg, solver, generator=torch.Generator().manual_seed(2), graphed=gs)
+    for p1, p2 in zip(b1.parameters(), b2.parameters()):
+        torch.testing.assert_close(p2, p1, rtol=1e-5, atol=1e-6)
+    assert m1["skipped_minibatches"] == m2["skipped_minibatches"]
+    assert abs(m1["approx_grad_frac"] - m2["approx_grad_frac"]) < 1e-12
+    assert abs(m1["surrogate"] - m2["surrogate"]) <= 1e-5 * max(1.0, abs(m1["surrogate"]))
