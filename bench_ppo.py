@@ -167,9 +167,11 @@ def train_mode(args):
 
     graphed = []
 
+    use_graph = world == 1 and not args.no_graph
+
     def iteration():
-        flat, stats = col.collect()
-        if not graphed and world == 1 and not args.no_graph:
+        flat, stats = col.collect_graphed() if use_graph else col.collect()
+        if not graphed and use_graph:
             mb = min(cfg.minibatch_size, flat["obs"].shape[0])
             ex = {"obs": flat["obs"][:mb], "actions": flat["actions"][:mb], "old_log_probs": flat["log_probs"][:mb],
                   "advantages": flat["advantages"][:mb].float(), "returns": flat["returns"][:mb].float(),
@@ -209,7 +211,7 @@ def train_mode(args):
                        "rollout_steps": args.rollout_steps, "minibatch_per_gpu": args.minibatch // world,
                        "parallelism": f"dp{world}"},
             "diffmpc_launches_per_iteration": (_lib.launch_count() - l0) / K,
-            "update_cuda_graph": bool(graphed),
+            "cuda_graphs": {"collection": use_graph, "minibatch_update": bool(graphed)},
             "mean_solver_iters": float(stats["solver_iters"]) / stats["solves"],
             "episodes_last_iteration": int(stats["episodes"]),
         }), flush=True)

@@ -48,6 +48,55 @@ class DeviceRollout:
         self.warm = torch.cat([ws.U[:, 1:], ws.U[:, -1:]], dim=1)
         return ws.U[:, 0].clone(), x_init, U_warm, ws.iters.clone()
 
+    # state carried from one collection to the next (rollout + environment)
+    _STATE = ("obs", "warm", "ep_return")
+    _ENV_STATE = ("x", "gate", "laps", "t", "done", "reason")
+
+    @torch.no_grad()
+    def collect_graphed(self, steps: int | None = None):
+        """``collect`` replayed from one CUDA graph holding the whole (steps x envs) loop:
+        actor -> batched DiffMPC solve -> critic -> action noise -> environment step, GAE.
+        The first call runs ``collect`` eagerly (creating the solver plan) and captures the
+        graph; every later call replays it. The carried state (observations, warm starts,
+        returns, environment state) lives in fixed buffers that the graph reads at its start
+        and writes back at its end; the two RNG streams are registered with the graph, so a
+        replay draws fresh noise exactly like an eager call would."""
+        S = steps or self.config.steps_per_update
+        g = getattr(self, "_graph", None)
+        if g is None or self._graph_steps != S:
+            out = self.collect(S)  # eager: creates the plan, warms the allocator
+            torch.cuda.synchronize(self.device)
+            self._static = {k: getattr(self, k).clone() for k in self._STATE}
+            self._static_env = {k: getattr(self.env, k).clone() for k in self._ENV_STATE}
+            for k, v in self._static.items():
+                setattr(self, k, v)
+            for k, v in self._static_env.items():
+                setattr(self.env, k, v)
+            g = torch.cuda.CUDAGraph()
+            g.register_generator_state(self.gen)
+            g.register_generator_state(self.env.gen)
+            side = torch.cuda.Stream(device=self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            steps0 = self.step_count
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    flat, stats = self.collect(S)
+                    for k, v in self._static.items():
+                        v.copy_(getattr(self, k))
+                    for k, v in self._static_env.items():
+                        v.copy_(getattr(self.env, k))
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            self.step_count = steps0
+            for k, v in self._static.items():
+                setattr(self, k, v)
+            for k, v in self._static_env.items():
+                setattr(self.env, k, v)
+            self._graph, self._graph_steps, self._graph_out = g, S, (flat, stats)
+            return out
+        g.replay()
+        self.step_count += S * self.N
+        return self._graph_out
+
     @torch.no_grad()
     def collect(self, steps: int | None = None):
         """One buffer of (steps, envs) transitions + GAE (trainer.py:276-329). Returns the

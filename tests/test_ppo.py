@@ -267,3 +267,35 @@ def test_ppo_update_with_graphed_step_matches_eager():
     assert m1["skipped_minibatches"] == m2["skipped_minibatches"]
     assert abs(m1["approx_grad_frac"] - m2["approx_grad_frac"]) < 1e-12
     assert abs(m1["surrogate"] - m2["surrogate"]) <= 1e-5 * max(1.0, abs(m1["surrogate"]))
+
+
+@pytest.mark.gpu
+def test_graphed_rollout_collection_matches_eager():
+    """DeviceRollout.collect_graphed (the whole steps x envs collection replayed from one CUDA
+    graph) produces the same transitions, advantages and statistics as eager collect calls
+    from the same seeds, collection after collection (carried state and RNG streams)."""
+    from paper_2605_29155_b200 import raceenv
+    from paper_2605_29155_b200.layer import MpcSolver
+    from paper_2605_29155_b200.rollout import DeviceRollout
+
+    dev = torch.device("cuda")
+    model = DynModel.planar_quadrotor(dt=0.05)
+    st = SolveSettings(T=5, u_min=0.0, u_max=2 * 0.5 * 9.81)
+    torch.manual_seed(0)
+    b = PolicyBundle("ac_mpc", raceenv.OBS_DIM, model, st, CostHeadScaling.for_model(model, 6),
+                     hidden=(64, 64)).to(dev)
+    cfg = ppo.TrainConfig(steps_per_update=8, minibatch_size=256, sgd_epochs=1)
+    cols = []
+    for _ in range(2):
+        env = raceenv.BatchedRaceEnv(raceenv.hairpin5(), model, 128, device=dev, seed=1)
+        cols.append(DeviceRollout(b, MpcSolver(model, st, device=dev), env, cfg, seed=2))
+    eager, graphed = cols
+    for it in range(4):
+        fa, sa = eager.collect()
+        fb, sb = graphed.collect_graphed()
+        for k in fa:
+            torch.testing.assert_close(fb[k], fa[k], rtol=0, atol=0, msg=f"collection {it}: {k}")
+        for k in ("episodes", "return_sum", "laps", "solver_iters"):
+            assert float(sb[k]) == float(sa[k]), (it, k)
+        fa = {k: v.clone() for k, v in fa.items()}
+    assert graphed.step_count == eager.step_count
