@@ -167,10 +167,11 @@ def train_mode(args):
 
     graphed = []
 
-    use_graph = world == 1 and not args.no_graph
+    graph_collect = not args.no_graph  # the collection has no collective: graphed at any N
+    use_graph = world == 1 and not args.no_graph  # the update carries the all-reduce
 
     def iteration():
-        flat, stats = col.collect_graphed() if use_graph else col.collect()
+        flat, stats = col.collect_graphed() if graph_collect else col.collect()
         if not graphed and use_graph:
             mb = min(cfg.minibatch_size, flat["obs"].shape[0])
             ex = {"obs": flat["obs"][:mb], "actions": flat["actions"][:mb], "old_log_probs": flat["log_probs"][:mb],
@@ -211,7 +212,7 @@ def train_mode(args):
                        "rollout_steps": args.rollout_steps, "minibatch_per_gpu": args.minibatch // world,
                        "parallelism": f"dp{world}"},
             "diffmpc_launches_per_iteration": (_lib.launch_count() - l0) / K,
-            "cuda_graphs": {"collection": use_graph, "minibatch_update": bool(graphed)},
+            "cuda_graphs": {"collection": graph_collect, "minibatch_update": bool(graphed)},
             "mean_solver_iters": float(stats["solver_iters"]) / stats["solves"],
             "episodes_last_iteration": int(stats["episodes"]),
         }), flush=True)
