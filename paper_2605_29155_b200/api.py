@@ -97,11 +97,11 @@ class BatchProblem:
 
 def _collect(model, settings, out) -> list:
     """Per-instance SolveResults from a device SolveOutput (ilqr.collect_result, ilqr.py:250-268)."""
-    X, U, J = out.X.cpu().numpy(), out.U.cpu().numpy(), out.J.cpu().numpy()
-    K, k = out.K.cpu().numpy(), out.k.cpu().numpy()
-    it, conv = out.iters.cpu().numpy(), out.converged.cpu().numpy()
-    div, ft = out.diverged.cpu().numpy(), out.fail_t.cpu().numpy()
-    ah = out.alpha_hist.cpu().numpy()
+    X, U, J = _solver.to_numpy(out.X), _solver.to_numpy(out.U), _solver.to_numpy(out.J)
+    K, k = _solver.to_numpy(out.K), _solver.to_numpy(out.k)
+    it, conv = _solver.to_numpy(out.iters), _solver.to_numpy(out.converged)
+    div, ft = _solver.to_numpy(out.diverged), _solver.to_numpy(out.fail_t)
+    ah = _solver.to_numpy(out.alpha_hist)
     lo, hi = settings.bounds_for(model.n_u)
     res = []
     for i in range(X.shape[0]):
@@ -149,7 +149,7 @@ def _grads(results, params, seeds, dtype, device):
     dX = np.stack([s.dL_dX for s in seeds])
     dU = np.stack([s.dL_dU for s in seeds])
     g = _solver.backward_raw(model, settings, C, c, X, U, dX, dU, dtype=dtype, device=device)
-    return g.dC.cpu().numpy(), g.dc.cpu().numpy(), g.dx0.cpu().numpy(), g.fail_t.cpu().numpy()
+    return _solver.to_numpy(g.dC), _solver.to_numpy(g.dc), _solver.to_numpy(g.dx0), _solver.to_numpy(g.fail_t)
 
 
 def backward(result: SolveResult, lin, p: StageCostParams, seed: BackwardSeed, dtype=torch.float64,

@@ -49,12 +49,12 @@ def latency_probe(B_list, T_list, reps=10, K=10, seed=0, model=None, layout="den
 
             def fwd():
                 out = solver.solve_raw(model, pb.settings, pb.x0, C, pb.c, pb.U_warm, dtype=torch.float64)
-                host = (out.X.cpu().numpy(), out.U.cpu().numpy(), out.J.cpu().numpy())
+                host = (solver.to_numpy(out.X), solver.to_numpy(out.U), solver.to_numpy(out.J))
                 return out, host
 
             def bwd(out):
                 g = solver.backward_raw(model, pb.settings, out.C, out.c, out.X, out.U, None, dU, dtype=torch.float64)
-                return g.dC.cpu().numpy(), g.dc.cpu().numpy(), g.dx0.cpu().numpy()
+                return solver.to_numpy(g.dC), solver.to_numpy(g.dc), solver.to_numpy(g.dx0)
 
             out, _ = fwd()  # warm-up round (excluded)
             bwd(out)

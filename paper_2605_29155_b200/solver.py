@@ -229,10 +229,22 @@ def backward_raw(model, settings, C, c, X, U, dLdX=None, dLdU=None, dLdJ=None, *
     return out
 
 
+def to_numpy(t):
+    """Device tensor -> numpy through page-locked memory (torch's caching host allocator):
+    one DMA at PCIe rate instead of a pageable copy (≈ 2-6 GB/s for the 0.1-0.2 GB dC of a
+    16k batch). The array views the pinned buffer, which returns to the cache when freed."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        return t.numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
+
+
 def dynamics(model, x, u, *, dtype=torch.float64, device=None, want_jac=True, theta=None):
     """Batched f(x,u) and Jacobians on the GPU; returns numpy arrays (N,nx), (N,nx,nx), (N,nx,nu)."""
-    cpu = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
-    return tuple(cpu(t) for t in dynamics_t(model, x, u, dtype=dtype, device=device, want_jac=want_jac,
+    return tuple(to_numpy(t) for t in dynamics_t(model, x, u, dtype=dtype, device=device, want_jac=want_jac,
                                            theta=theta))
 
 
