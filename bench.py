@@ -58,11 +58,15 @@ def dist_env():
     return rank, world, local
 
 
-def workload(args, seed):
-    from paper_2605_29155_b200 import DynModel, problems
+def workload(args, rank=0, world=1):
+    """Rank `rank`'s contiguous shard (shard.shard_range) of ONE global batch of
+    world x batch hover problems (seed 0): the sharding the multi-GPU tests cover."""
+    from paper_2605_29155_b200 import DynModel, problems, shard
     model = DynModel.quadrotor(dt=0.05)
-    pb = problems.hover_problem(model, args.batch, args.T, seed=seed)
-    return pb
+    Bg = args.batch * world
+    pb = problems.hover_problem(model, Bg, args.T, seed=0)
+    lo, hi = shard.shard_range(Bg, rank, world)
+    return pb.slice(lo, hi)
 
 
 def config(args, world):
@@ -150,7 +154,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    pb = workload(args, seed=0)
+    pb = workload(args)
     rates = []
     for _ in range(max(1, args.warmup // 3)):
         cpu_oracle_rate(pb, seconds=2.0)
@@ -187,7 +191,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("gloo" if share else "nccl", **({} if share else {"device_id": dev}))
     dtype = torch.float32 if args.dtype == "f32" else torch.float64
-    pb = workload(args, seed=rank)
+    pb = workload(args, rank, world)
     model, st = pb.model, pb.settings
     B, T, n, m = args.batch, args.T, model.n_x, model.n_u
     Ch = pb.dense_C() if args.layout == "dense" else pb.diag
@@ -355,6 +359,34 @@ def run_ours(args):
              "fwd_tflops": roofline.fwd_flops(n, m, T, it0, len(st.alphas)) / (fx_f * 1e-3) / 1e12,
              "how": "conv_tol=0, K_max=10, same inputs; per-rank device time, median of 10"}
 
+    # ---- the same step in float64 (the reference's precision), device-timed ----
+    f64leg = None
+    if dtype == torch.float32 and rank == 0:
+        d64 = {k: v.to(torch.float64) for k, v in dev_in.items()}
+        ev64 = []
+        for k in range(3 + 5):
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            o64 = solver.solve_raw(model, st, d64["x0"], d64["C"], d64["c"], d64["U_warm"], dtype=torch.float64)
+            e1.record(stream)
+            solver.backward_raw(model, st, d64["C"], d64["c"], o64.X, o64.U, None, d64["dLdU"],
+                                dtype=torch.float64)
+            e2.record(stream)
+            if k >= 3:
+                ev64.append((e0, e1, e2))
+        torch.cuda.synchronize()
+        f64_f = float(np.median([a.elapsed_time(b) for a, b, _ in ev64]))
+        f64_b = float(np.median([b.elapsed_time(c) for _, b, c in ev64]))
+        f64leg = {"dtype": "f64", "value": B / ((f64_f + f64_b) * 1e-3), "unit": "solves/s",
+                  "forward_ms": f64_f, "backward_ms": f64_b,
+                  "how": "same inputs and settings, float64 kernels; rank 0, median of 5 after 3 warm-up"}
+        del d64, o64
+
+    # ---- self-check of the timed outputs against the oracle (untimed, bounded sample) ----
+    parity = None
+    if rank == 0:
+        parity = self_check(pb, out, g, dtype, args.layout)
+
     # ---- roofline of the dominant kernel (the fused forward) ----
     F = roofline.fwd_flops(n, m, T, it_np, len(st.alphas))
     achieved = F / (fwd_ms * 1e-3) / 1e12
@@ -388,10 +420,15 @@ def run_ours(args):
                 "fixed_work": dict(fixed, roofline_frac=fixed["fwd_tflops"] / peak),
                 "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "traffic": traffic, "kernel": "ilqr_forward_kernel",
+                             "traffic_source": "profiles/traffic.json: dram__bytes_read.sum + "
+                                               "dram__bytes_write.sum of this kernel from the committed "
+                                               "ncu --set full capture (not measured in this run)",
                              "peak_source": peak_kind,
                              "algorithmic_bytes": bytes_fwd,
                              "hbm_gbs": bytes_fwd / (fwd_ms * 1e-3) / 1e9},
-                "clocks": clk.summary()}
+                "clocks": clk.summary(),
+                "parity": parity,
+                "reference_precision": f64leg}
         if not args.no_cpu_baseline and world == 1:
             r, thr, sample = cpu_oracle_rate(pb, seconds=12.0)
             line["cpu_baseline"] = {"value": r, "unit": "solves/s", "cores": thr, "kind": "port",
@@ -400,6 +437,45 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def self_check(pb, out, g, dtype, layout, n=512):
+    """The timed step's own outputs for the first n problems of the shard vs the C oracle
+    on identical (dtype-rounded) inputs: iteration counts, clamp masks and the worst
+    per-instance relative error of X, U, J, dC, dc, dx0 (north_star gate: 1e-4 in f32)."""
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    from paper_2605_29155_b200 import _abi
+    n = min(n, pb.B)
+    rnd = (lambda a: np.asarray(a, np.float32).astype(np.float64)) if dtype == torch.float32 else np.asarray
+    cost = pb.dense_C()[:n] if layout == "dense" else pb.diag[:n]
+    lay = _abi.COST_DENSE if layout == "dense" else _abi.COST_DIAG
+    x0, C, c, Uw = rnd(pb.x0[:n]), rnd(cost), rnd(pb.c[:n]), rnd(pb.U_warm[:n])
+    dU = np.zeros((n, pb.settings.T, pb.model.n_u))
+    dU[:, 0, :] = 1.0
+    th = len(os.sched_getaffinity(0))
+    ref = oracle.forward(pb.model, pb.settings, x0, C, c, Uw, layout=lay, threads=th)
+    rg = oracle.backward(pb.model, pb.settings, C, c, ref["X"], ref["U"], None, dU, layout=lay, threads=th,
+                         want_theta=False)
+
+    def rel(a, b):
+        a = np.asarray(a, np.float64).reshape(n, -1)
+        b = np.asarray(b, np.float64).reshape(n, -1)
+        return float((np.abs(a - b).max(1) / np.maximum(1.0, np.abs(b).max(1))).max())
+
+    get = lambda t: t[:n].detach().cpu().numpy()  # noqa: E731
+    err = {"X": rel(get(out.X), ref["X"]), "U": rel(get(out.U), ref["U"]),
+           "J": rel(get(out.J)[:, None], ref["J"][:, None]), "dC": rel(get(g.dC), rg["dC"]),
+           "dc": rel(get(g.dc), rg["dc"]), "dx0": rel(get(g.dx0), rg["dx0"])}
+    it_eq = bool(np.array_equal(get(out.iters), ref["iters"]))
+    cl_eq = bool(np.array_equal(get(out.clamped).astype(np.uint8), ref["clamped"]))
+    tol = 1e-4 if dtype == torch.float32 else 1e-9
+    return {"checked": n, "oracle": "oracle/ (C, f64, pinned bit-exact to the reference goldens)",
+            "iters_identical": it_eq, "clamp_masks_identical": cl_eq, "max_rel_err": err, "tol": tol,
+            "pass": it_eq and cl_eq and max(err.values()) <= tol}
 
 
 def pcie_bidir_gbs(dev, mb=64, reps=5):

@@ -85,12 +85,12 @@ def main():
              "advantages": torch.randn(B, device=dev, generator=g), "returns": torch.randn(B, device=dev, generator=g),
              "x_init": x_init, "U_warm": U_warm}
     sink = {}
-    use_graph = world == 1 and not args.no_graph
+    use_graph = not args.no_graph  # NCCL all-reduce captured in the graph; gloo dry-run reduces eagerly
     if use_graph:
-        gstep = ppo.GraphedMinibatchStep(bundle, opt, batch, cfg, solver)
+        gstep = ppo.GraphedMinibatchStep(bundle, opt, batch, cfg, solver, reducer=reducer)
 
         def step(sink_):
-            gstep(batch)
+            gstep(batch, sink_)
     else:
         def step(sink_):
             ppo.minibatch_step(bundle, opt, batch, cfg, solver, reducer, sink_)
@@ -112,18 +112,22 @@ def main():
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    launches = gstep.diffmpc_launches if use_graph else (_lib.launch_count() - l0) / args.steps
+    launches = (_lib.launch_count() - l0) / args.steps  # graph replays included (_lib.note_graph_replay)
     if rank == 0:
         print(json.dumps({
-            "metric": "AC-MPC PPO minibatch steps/s (DiffMPC actor fwd+bwd + NCCL grad all-reduce)",
+            "metric": "AC-MPC PPO minibatch steps/s (DiffMPC actor fwd+bwd + grad all-reduce at N>1)",
             "value": 1e3 / ms, "unit": "steps/s", "samples_per_s": world * B * 1e3 / ms,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "dtype": "f32", "data": "synthetic",
             "config": {"workload": "AC-MPC PPO step, quadrotor13 diag cost", "T": T, "minibatch_per_gpu": B,
                        "global_minibatch": B * world, "params": sum(p.numel() for p in bundle.parameters()),
-                       "allreduce_bytes": reducer.nbytes, "parallelism": f"dp{world}"},
+                       "allreduce_bytes": reducer.nbytes if world > 1 else 0,
+                       "collective": (f"one flat all-reduce per step ({dist.get_backend()})" if world > 1
+                                      else "none (one process)"),
+                       "parallelism": f"dp{world}"},
             "diffmpc_launches_per_step": launches,
             "cuda_graph": use_graph,
+            "allreduce_in_graph": bool(use_graph and world > 1 and gstep.in_graph),
             "mean_solver_iters": (float(sink.get("iterations", 0)) / max(1, sink.get("solves", 1))) if sink else None,
         }), flush=True)
     if world > 1:
@@ -168,18 +172,20 @@ def train_mode(args):
     graphed = []
 
     graph_collect = not args.no_graph  # the collection has no collective: graphed at any N
-    use_graph = world == 1 and not args.no_graph  # the update carries the all-reduce
+    use_graph = not args.no_graph  # the update graph carries the NCCL all-reduce at N>1
 
     def iteration():
         flat, stats = col.collect_graphed() if graph_collect else col.collect()
         if not graphed and use_graph:
-            mb = min(cfg.minibatch_size, flat["obs"].shape[0])
+            # rank-local buffers: each rank trains on all of its own transitions in
+            # minibatches of minibatch/world samples (ppo_update data="sharded")
+            mb = max(1, min(cfg.minibatch_size, flat["obs"].shape[0] * world) // world)
             ex = {"obs": flat["obs"][:mb], "actions": flat["actions"][:mb], "old_log_probs": flat["log_probs"][:mb],
                   "advantages": flat["advantages"][:mb].float(), "returns": flat["returns"][:mb].float(),
                   "x_init": flat["x_init"][:mb], "U_warm": flat["U_warm"][:mb]}
-            graphed.append(ppo.GraphedMinibatchStep(bundle, opt, ex, cfg, solver))
+            graphed.append(ppo.GraphedMinibatchStep(bundle, opt, ex, cfg, solver, reducer=reducer))
         m = ppo.ppo_update(flat, bundle, opt, cfg, solver, generator=gen, reducer=reducer, rank=rank, world=world,
-                           graphed=graphed[0] if graphed else None)
+                           graphed=graphed[0] if graphed else None, data="sharded")
         return stats, m
 
     for _ in range(max(1, args.warmup // 3)):
@@ -191,8 +197,10 @@ def train_mode(args):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     K = max(2, args.steps // 10)
     a.record()
+    trained = 0
     for _ in range(K):
         stats, m = iteration()
+        trained += m["samples_trained"]
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / K
@@ -213,6 +221,7 @@ def train_mode(args):
                        "parallelism": f"dp{world}"},
             "diffmpc_launches_per_iteration": (_lib.launch_count() - l0) / K,
             "cuda_graphs": {"collection": graph_collect, "minibatch_update": bool(graphed)},
+            "samples_trained_per_iteration": trained / K,
             "mean_solver_iters": float(stats["solver_iters"]) / stats["solves"],
             "episodes_last_iteration": int(stats["episodes"]),
         }), flush=True)

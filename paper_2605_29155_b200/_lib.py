@@ -73,8 +73,18 @@ def check(rc: int):
         raise ConfigError(msg)
 
 
+_replayed = 0  # DiffMPC kernels executed by CUDA-graph replays (invisible to the C counter)
+
+
+def note_graph_replay(n: int):
+    """Account the n DiffMPC launches a captured graph performs per replay."""
+    global _replayed
+    _replayed += int(n)
+
+
 def launch_count() -> int:
-    return int(lib().diffmpc_launch_count())
+    """DiffMPC kernels launched so far: ABI calls (captures included) + graph replays."""
+    return int(lib().diffmpc_launch_count()) + _replayed
 
 
 def supported(kind: int, nx: int, nu: int) -> bool:

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   // Every group claims its own next problem with one atomicAdd by its lane 0 and a
   // group-masked broadcast. (A warp-wide claim — one full-mask shuffle reached by the two
   // groups of a warp at different times, while the other group executes group-masked
-  // collectives — intermittently lost the second group's problem; tools/stress_b7.py.)
+  // collectives — intermittently lost the second group's problem; tools/stress.py small.)
   auto claim = [&]() -> int {
     int u = 0;
     if (lane == 0) u = atomicAdd(args.ctr, 1);
@@ -338,6 +338,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         fail_t = t;
         active = 0;
         diverged = 1;  // rollout_failed (ilqr.py:196-200)
+        // rows past the failure keep the reference Workspace's zero init (ilqr.py:84-133),
+        // not states of the group's previous problem
+        for (int e = lane; e < (T - 1 - t) * XLD; e += G) Xn[(t + 2) * XLD + e] = 0.0;
+        __syncwarp(gm);
         break;
       }
     }

@@ -264,6 +264,8 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
       }
       if (!fin) {
         fail = t;
+        // rows past the failure keep the reference Workspace's zero init (ilqr.py:84-133)
+        for (int e = lane; e < (T - 1 - t) * XLD; e += 32) Xbuf(0)[(t + 2) * XLD + e] = 0.0;
         break;
       }
     }

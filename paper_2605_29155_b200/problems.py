@@ -30,6 +30,11 @@ class Problem:
     def B(self):
         return self.x0.shape[0]
 
+    def slice(self, lo: int, hi: int) -> "Problem":
+        """Problems [lo, hi) of the batch (a rank's shard of a global batch)."""
+        return Problem(self.model, self.settings, self.x0[lo:hi], self.diag[lo:hi], self.c[lo:hi],
+                       self.U_warm[lo:hi])
+
     def dense_C(self) -> np.ndarray:
         """(B, T, nz, nz) with the diagonal placed as StageCostParams.from_diag does."""
         B, T, nz = self.diag.shape

@@ -78,6 +78,8 @@ class DeviceRollout:
             side = torch.cuda.Stream(device=self.device)
             side.wait_stream(torch.cuda.current_stream(self.device))
             steps0 = self.step_count
+            from . import _lib
+            l0 = _lib.launch_count()
             with torch.cuda.stream(side):
                 with torch.cuda.graph(g, stream=side):
                     flat, stats = self.collect(S)
@@ -91,9 +93,12 @@ class DeviceRollout:
                 setattr(self, k, v)
             for k, v in self._static_env.items():
                 setattr(self.env, k, v)
+            self.graph_launches = _lib.launch_count() - l0  # DiffMPC kernels per replay
             self._graph, self._graph_steps, self._graph_out = g, S, (flat, stats)
             return out
         g.replay()
+        from . import _lib
+        _lib.note_graph_replay(self.graph_launches)
         self.step_count += S * self.N
         return self._graph_out
 

@@ -65,9 +65,22 @@ def _theta(model, theta, dtype, device, B):
     return th, model.n_theta
 
 
-def _stream(stream=None) -> int:
-    s = torch.cuda.current_stream() if stream is None else stream
+def _stream(stream=None, device=None) -> int:
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return s.cuda_stream
+
+
+def _on(dev, stream):
+    """Run a call with `dev` current and, when given, `stream` as torch's current stream, so
+    every allocation of the call (outputs, converted inputs, workspace) is made on the stream
+    the kernel runs on and the caching allocator cannot recycle it under the running kernel."""
+    import contextlib
+
+    ctx = contextlib.ExitStack()
+    ctx.enter_context(torch.cuda.device(dev))
+    if stream is not None:
+        ctx.enter_context(torch.cuda.stream(stream))
+    return ctx
 
 
 def _layout(C, B, T, nz) -> int:
@@ -131,6 +144,11 @@ def solve_raw(model, settings, x_init, C, c, U_warm, *, dtype=torch.float32, dev
     if dtype not in _DT:
         raise ConfigError(f"dtype must be float32 or float64, got {dtype}")
     dev = _device(device)
+    with _on(dev, stream):
+        return _solve_raw(model, settings, x_init, C, c, U_warm, dtype, dev, theta, want_gains, kernel)
+
+
+def _solve_raw(model, settings, x_init, C, c, U_warm, dtype, dev, theta, want_gains, kernel):
     T, nx, nu = settings.T, model.n_x, model.n_u
     nz = nx + nu
     x_init = _as(x_init, dtype, dev, name="x_init")
@@ -170,8 +188,7 @@ def solve_raw(model, settings, x_init, C, c, U_warm, *, dtype=torch.float32, dev
     ws = torch.empty((wsb,), dtype=torch.uint8, device=dev)
     io.workspace, io.workspace_bytes = P(ws), wsb
     fn = getattr(L, f"diffmpc_forward_{_DT[dtype]}")
-    with torch.cuda.device(dev):
-        _lib.check(fn(ctypes.byref(p), ctypes.byref(io), _stream(stream)))
+    _lib.check(fn(ctypes.byref(p), ctypes.byref(io), _stream()))
     out.converged = out.converged.bool()
     out.diverged = out.diverged.bool()
     out.clamped = out.clamped.bool()
@@ -191,6 +208,12 @@ def backward_raw(model, settings, C, c, X, U, dLdX=None, dLdU=None, dLdJ=None, *
     dev = _device(device)
     if dtype is None:
         dtype = X.dtype if isinstance(X, torch.Tensor) else torch.float32
+    with _on(dev, stream):
+        return _backward_raw(model, settings, C, c, X, U, dLdX, dLdU, dLdJ, dtype, dev, theta, want_theta,
+                             want_traj)
+
+
+def _backward_raw(model, settings, C, c, X, U, dLdX, dLdU, dLdJ, dtype, dev, theta, want_theta, want_traj):
     T, nx, nu = settings.T, model.n_x, model.n_u
     nz = nx + nu
     X = _as(X, dtype, dev, name="X")
@@ -224,8 +247,7 @@ def backward_raw(model, settings, C, c, X, U, dLdX=None, dLdU=None, dLdJ=None, *
     io.dC, io.dc, io.dx0, io.dtheta = P(out.dC), P(out.dc), P(out.dx0), P(out.dtheta)
     io.dX, io.dU, io.fail_t = P(out.dX), P(out.dU), P(out.fail_t)
     fn = getattr(_lib.lib(), f"diffmpc_backward_{_DT[dtype]}")
-    with torch.cuda.device(dev):
-        _lib.check(fn(ctypes.byref(p), ctypes.byref(io), _stream(stream)))
+    _lib.check(fn(ctypes.byref(p), ctypes.byref(io), _stream()))
     return out
 
 
@@ -343,7 +365,9 @@ class SolvePlan:
         io.C = self._check(C, self.C_shape, "C")
         io.c = self._check(c, (self.B, T, nx + nu), "c")
         io.U_warm = self._check(U_warm, (self.B, T, nu), "U_warm")
-        _lib.check(self._fwd(ctypes.byref(self.p), ctypes.byref(io), _stream(stream)))
+        # the plan's buffers are owned by the plan (no per-call allocation); the launch goes
+        # to `stream` or the current stream of the PLAN's device
+        _lib.check(self._fwd(ctypes.byref(self.p), ctypes.byref(io), _stream(stream, self.dev)))
         self.out.C, self.out.c = C, c
         return self.out
 
@@ -357,5 +381,5 @@ class SolvePlan:
         io.dLdX = None if dLdX is None else self._check(dLdX, (self.B, T + 1, nx), "dL/dX")
         io.dLdU = None if dLdU is None else self._check(dLdU, (self.B, T, nu), "dL/dU")
         io.dLdJ = None if dLdJ is None else self._check(dLdJ, (self.B,), "dL/dJ")
-        _lib.check(self._bwd(ctypes.byref(self.p), ctypes.byref(io), _stream(stream)))
+        _lib.check(self._bwd(ctypes.byref(self.p), ctypes.byref(io), _stream(stream, self.dev)))
         return self.grad

@@ -26,20 +26,26 @@ def test_solve_layer_matches_reference_semantics(dtype):
     u0 = MpcSolveLayer.apply(diag, cvec, solver, pb.x0, pb.U_warm, sink)
     w = torch.randn(32, 4, dtype=dtype, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
     (u0 * w).sum().backward()
-    ref = oracle.forward(model, pb.settings, pb.x0, pb.dense_C(), pb.c, pb.U_warm)
+    # the oracle solves exactly the problem the kernel saw (f32 kernels: f32-rounded inputs)
+    rnd = (lambda a: np.asarray(a, np.float32).astype(np.float64)) if dtype == torch.float32 else np.asarray
+    x0, C, c, Uw = rnd(pb.x0), rnd(pb.dense_C()), rnd(pb.c), rnd(pb.U_warm)
+    ref = oracle.forward(model, pb.settings, x0, C, c, Uw)
     seed = np.zeros((32, 10, 4))
     seed[:, 0] = w.double().cpu().numpy()
-    rb = oracle.backward(model, pb.settings, pb.dense_C(), pb.c, ref["X"], ref["U"], None, seed, want_theta=False)
-    same = solver.solve_diag(pb.x0, pb.diag, pb.c, pb.U_warm)[1].cpu().numpy() == ref["iters"]
+    rb = oracle.backward(model, pb.settings, C, c, ref["X"], ref["U"], None, rnd(seed), want_theta=False)
+    iters = solver.solve_diag(pb.x0, pb.diag, pb.c, pb.U_warm)[1].cpu().numpy()
+    np.testing.assert_array_equal(iters, ref["iters"])
     tol = 1e-9 if dtype == torch.float64 else 1e-4
     idx = np.arange(17)
     assert sink["solves"] == 32
-    e = np.abs(u0.detach().double().cpu().numpy()[same] - ref["U"][same, 0]).max()
-    assert e <= tol * 10
-    gd = diag.grad.double().cpu().numpy()[same]
-    gc = cvec.grad.double().cpu().numpy()[same]
-    assert np.abs(gd - rb["dC"][same][:, :, idx, idx]).max() <= tol * 10 * max(1, np.abs(gd).max())
-    assert np.abs(gc - rb["dc"][same]).max() <= tol * 10 * max(1, np.abs(gc).max())
+
+    def rel(a, b):  # per instance, SURVEY.md §8(c)
+        a, b = a.reshape(a.shape[0], -1), b.reshape(b.shape[0], -1)
+        return (np.abs(a - b).max(1) / np.maximum(1.0, np.abs(b).max(1))).max()
+
+    assert rel(u0.detach().double().cpu().numpy(), ref["U"][:, 0]) <= tol
+    assert rel(diag.grad.double().cpu().numpy(), rb["dC"][:, :, idx, idx]) <= tol
+    assert rel(cvec.grad.double().cpu().numpy(), rb["dc"]) <= tol
 
 
 def test_layer_gradient_matches_finite_differences():

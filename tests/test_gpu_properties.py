@@ -123,9 +123,12 @@ def test_dtheta_and_cost_gradients_match_oracle(kind, dtype):
     ref = oracle.forward(model, s, x0, C, c, Uw)
     n, m = model.n_x, model.n_u
     sX, sU, sJ = rng.normal(size=(Bn, T + 1, n)), rng.normal(size=(Bn, T, m)), rng.normal(size=Bn)
-    rb = oracle.backward(model, s, C, c, ref["X"], ref["U"], sX, sU, sJ)
-    g = solver.backward_raw(model, s, C, c, ref["X"], ref["U"], sX, sU, sJ, dtype=dtype, want_theta=True)
-    tol = 1e-9 if dtype == torch.float64 else 2e-4
+    # identical inputs on both sides (f32 kernel: f32-rounded)
+    rnd = (lambda a: np.asarray(a, np.float32).astype(np.float64)) if dtype == torch.float32 else np.asarray
+    C, c, X, U, sX, sU, sJ = (rnd(a) for a in (C, c, ref["X"], ref["U"], sX, sU, sJ))
+    rb = oracle.backward(model, s, C, c, X, U, sX, sU, sJ)
+    g = solver.backward_raw(model, s, C, c, X, U, sX, sU, sJ, dtype=dtype, want_theta=True)
+    tol = 1e-9 if dtype == torch.float64 else 1e-4
     ok = rb["fail_t"] < 0
     for key in ("dtheta", "dC", "dc", "dx0"):
         got = getattr(g, key).cpu().numpy()[ok]

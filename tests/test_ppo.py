@@ -106,6 +106,78 @@ def test_data_parallel_update_matches_single_process():
     assert nbytes == 4 * sum(p.numel() for p in b.parameters())
 
 
+def _worker_sharded(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, model, st = _bundle()
+    cfg = ppo.TrainConfig(mode="ac_mlp", minibatch_size=64, sgd_epochs=2)
+    opt = torch.optim.Adam(b.parameters(), lr=1e-3)
+    red = ppo.GradAllReduce(b.parameters())
+    # every rank trains on its OWN buffer (its environments' transitions)
+    m = ppo.ppo_update(_buffer(96, model, st.T, seed=10 + rank), b, opt, cfg,
+                       generator=torch.Generator().manual_seed(3), reducer=red, rank=rank, world=world,
+                       data="sharded")
+    flat = torch.cat([p.detach().reshape(-1) for p in b.parameters()])
+    parts = [torch.empty_like(flat) for _ in range(world)]
+    dist.all_gather(parts, flat)
+    if rank == 0:
+        q.put((parts[0].numpy(), parts[1].numpy(), m["samples_trained"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_data_parallel_update_on_rank_local_buffers():
+    """with rank-local rollout buffers every collected transition is trained on.
+    World-2 gloo with DIFFERENT buffers per rank equals one process stepping on the union
+    of the two ranks' minibatch shards (global advantage normalisation)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sharded, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    p0, p1, trained = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    np.testing.assert_array_equal(p0, p1)
+    assert trained == 2 * 96 * 2  # both buffers, both epochs
+    b, model, st = _bundle()
+    cfg = ppo.TrainConfig(mode="ac_mlp", minibatch_size=64, sgd_epochs=2)
+    opt = torch.optim.Adam(b.parameters(), lr=1e-3)
+    bufs = [_buffer(96, model, st.T, seed=10 + r) for r in range(2)]
+    adv = torch.cat([x["advantages"] for x in bufs])
+    mean, std = adv.mean(), adv.std()
+    gen = torch.Generator().manual_seed(3)
+    for _ in range(cfg.sgd_epochs):
+        perm = torch.randperm(96, generator=gen)
+        for s0 in range(0, 96, 32):
+            sel = perm[s0:s0 + 32]
+            batch = {"obs": torch.cat([x["obs"][sel] for x in bufs]),
+                     "actions": torch.cat([x["actions"][sel] for x in bufs]),
+                     "old_log_probs": torch.cat([x["log_probs"][sel] for x in bufs]),
+                     "advantages": (torch.cat([x["advantages"][sel] for x in bufs]) - mean) / (std + 1e-8),
+                     "returns": torch.cat([x["returns"][sel] for x in bufs])}
+            ppo.minibatch_step(b, opt, batch, cfg)
+    ref = torch.cat([p.detach().reshape(-1) for p in b.parameters()]).numpy()
+    np.testing.assert_allclose(p0, ref, rtol=2e-5, atol=2e-6)
+
+
+def test_grad_bucket_views_survive_zero_grad():
+    """The reducer's bucket views are re-bound after optimizer.zero_grad(set_to_none=True)."""
+    b, model, st = _bundle()
+    red = ppo.GradAllReduce(b.parameters())
+    opt = torch.optim.Adam(b.parameters(), lr=1e-3)
+    red.zero_()
+    assert all(p.grad is v for p, v in zip(red.params, red.views))
+    opt.zero_grad()
+    assert all(p.grad is None for p in red.params)
+    red.bind()
+    out = b.critic(torch.randn(4, 13)).sum()
+    out.backward()
+    assert all(p.grad is v for p, v in zip(red.params, red.views))
+    assert float(red.flat[:red.n].abs().sum()) > 0.0
+
+
 def test_ac_mpc_bundle_sizes_match_reference_formula():
     """Actor head T*2*n_z and the flat bucket size quoted in SURVEY.md §8(e)."""
     model = DynModel.quadrotor(dt=0.05)
@@ -299,3 +371,77 @@ def test_graphed_rollout_collection_matches_eager():
             assert float(sb[k]) == float(sa[k]), (it, k)
         fa = {k: v.clone() for k, v in fa.items()}
     assert graphed.step_count == eager.step_count
+
+
+@pytest.mark.gpu
+def test_graphed_update_with_partial_last_minibatch():
+    """n % minibatch_size != 0 sends the last minibatch through the eager step,
+    whose zero_grad(set_to_none) drops the .grad tensors; the graphed step re-binds its bucket
+    views before every replay, so parameters still match the all-eager update."""
+    import copy
+
+    from paper_2605_29155_b200 import problems
+    from paper_2605_29155_b200.layer import MpcSolver
+
+    dev = torch.device("cuda")
+    model = DynModel.quadrotor(dt=0.05)
+    n, T, mb = 300, 10, 128
+    pb = problems.hover_problem(model, n, T, seed=4)
+    torch.manual_seed(0)
+    b1 = PolicyBundle("ac_mpc", 13, model, pb.settings, CostHeadScaling.for_model(model, 13),
+                      hidden=(64, 64)).to(dev)
+    b2 = copy.deepcopy(b1)
+    solver = MpcSolver(model, pb.settings, device=dev)
+    cfg = ppo.TrainConfig(minibatch_size=mb, sgd_epochs=3)
+    o1 = torch.optim.Adam(b1.parameters(), lr=cfg.lr_start)
+    o2 = torch.optim.Adam(b2.parameters(), lr=cfg.lr_start)
+    g = torch.Generator(device=dev).manual_seed(9)
+    x = torch.tensor(pb.x0, dtype=torch.float32, device=dev)
+    buf = {"obs": x, "actions": torch.randn((n, 4), device=dev, generator=g),
+           "log_probs": torch.randn(n, device=dev, generator=g) - 3.0,
+           "advantages": torch.randn(n, device=dev, generator=g, dtype=torch.float64),
+           "returns": torch.randn(n, device=dev, generator=g, dtype=torch.float64),
+           "x_init": x, "U_warm": torch.tensor(pb.U_warm, dtype=torch.float32, device=dev)}
+    ppo.ppo_update(buf, b1, o1, cfg, solver, generator=torch.Generator().manual_seed(2))
+    ex = {"obs": x[:mb], "actions": buf["actions"][:mb], "old_log_probs": buf["log_probs"][:mb],
+          "advantages": buf["advantages"][:mb].float(), "returns": buf["returns"][:mb].float(),
+          "x_init": x[:mb], "U_warm": buf["U_warm"][:mb]}
+    gs = ppo.GraphedMinibatchStep(b2, o2, ex, cfg, solver)
+    ppo.ppo_update(buf, b2, o2, cfg, solver, generator=torch.Generator().manual_seed(2), graphed=gs)
+    for p1, p2 in zip(b1.parameters(), b2.parameters()):
+        torch.testing.assert_close(p2, p1, rtol=1e-5, atol=1e-6)
+    assert all(p.grad is v for p, v in zip(gs.reducer.params, gs.reducer.views))
+
+
+@pytest.mark.gpu
+def test_nccl_allreduce_captures_into_cuda_graph():
+    """The mechanism GraphedMinibatchStep relies on at N>1: an NCCL all-reduce of the flat
+    bucket captured in a CUDA graph and replayed (world 1 on the one-GPU box)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        buf = torch.ones(1024, device=dev)
+        dist.all_reduce(buf)  # communicator init outside the capture
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(gr):
+                buf.mul_(2.0)
+                dist.all_reduce(buf)
+                buf.add_(1.0)
+        torch.cuda.current_stream().wait_stream(side)
+        buf.fill_(1.0)
+        for _ in range(3):
+            gr.replay()
+        torch.cuda.synchronize()
+        assert float(buf[0]) == 15.0  # ((1*2+1)*2+1)*2+1
+    finally:
+        dist.destroy_process_group()

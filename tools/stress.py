@@ -1,5 +1,9 @@
-"""Repeatability stress across models, layouts, dtypes and both forward mappings, plus the
-backward (development aid): any mismatch between repeated launches is a race."""
+"""Repeatability stress (development aid): any mismatch between repeated launches is a race.
+
+python tools/stress.py [all|small]
+  all    models x layouts x dtypes x both forward mappings, plus the backward
+  small  the throughput forward on every batch size 1..40 and a few odd larger ones
+         (group-claim races show up on small / odd batches)"""
 import os
 import sys
 
@@ -12,7 +16,8 @@ from paper_2605_29155_b200 import DynModel, SolveSettings, problems, solver  # n
 models = [("quad13", DynModel.quadrotor()), ("planar", DynModel.planar_quadrotor(dt=0.05)),
           ("lin32", DynModel.linear(np.eye(3) + 0.05, 0.3 * np.ones((3, 2))))]
 bad = 0
-for name, m in models:
+mode = sys.argv[1] if len(sys.argv) > 1 else "all"
+for name, m in (models if mode == "all" else []):
     for layout in ("dense", "diag"):
         for dtype in (torch.float32, torch.float64):
             for kernel in ("throughput", "latency"):
@@ -41,4 +46,18 @@ for name, m in models:
                         if not ok:
                             bad += 1
                             print("MISMATCH", name, layout, dtype, kernel, "B", B, "rep", rep, flush=True)
+if mode == "small":
+    m = DynModel.quadrotor()
+    for B in list(range(1, 41)) + [63, 65, 127, 129, 300, 1000]:
+        pb = problems.random_problem(m, B, 10, seed=B)
+        C = pb.dense_C()
+        ref = solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="throughput")
+        for rep in range(10):
+            o = solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="throughput")
+            if not (torch.equal(o.iters, ref.iters) and torch.equal(o.U, ref.U) and torch.equal(o.X, ref.X)):
+                bad += 1
+                print("mismatch B", B, "rep", rep, flush=True)
+        if (ref.iters < 0).any() or (ref.iters > pb.settings.K_max).any():
+            bad += 1
+            print("garbage iters B", B, ref.iters.tolist()[:8], flush=True)
 print("bad", bad)
