@@ -46,30 +46,48 @@ def round_inputs(arrs, dtype):
     return [None if a is None else np.asarray(a, np.float32).astype(np.float64) for a in arrs]
 
 
-def decision_margin(ref, i, conv_tol):
-    """Oracle-side margin of the convergence decision of instance i at its last iteration:
-    (rel - conv_tol) / conv_tol, where rel = |J_prev - J| / max(1, |J_prev|)
-    (ilqr.py:233-238). Small |margin| = the reference decided within round-off."""
-    it = int(ref["iters"][i])
-    if it == 0:
+def _rel_steps(Jh, iters):
+    """rel_k = |J_{k-1} - J_k| / max(1, |J_{k-1}|) for k = 1..iters (ilqr.py:233-238)."""
+    Jh = np.asarray(Jh, np.float64)
+    k = np.arange(1, int(iters) + 1)
+    return np.abs(Jh[k - 1] - Jh[k]) / np.maximum(1.0, np.abs(Jh[k - 1]))
+
+
+def decision_margin(ref, i, conv_tol, upto=None):
+    """Oracle-side margin of instance i's convergence decisions: min over its iterations of
+    |rel_k - conv_tol| / conv_tol, from the oracle's float64 J history. A small margin means
+    the reference itself decided within round-off of the threshold, so a kernel computing in
+    another precision can legitimately take the other branch."""
+    if conv_tol <= 0:
         return float("nan")
-    Jh = ref["J_hist"][i]
-    jp, jn = Jh[it - 1], Jh[it]
-    rel = abs(jp - jn) / max(1.0, abs(jp))
-    return (rel - conv_tol) / conv_tol if conv_tol > 0 else float("nan")
+    n = int(ref["iters"][i]) if upto is None else int(upto)
+    if n == 0:
+        return float("inf")
+    r = _rel_steps(ref["J_hist"][i], n)
+    return float(np.min(np.abs(r - conv_tol)) / conv_tol)
+
+
+# f32 kernels: an iteration-count flip is accepted only where the reference decided within
+# this margin of conv_tol (the f32 J agrees with the oracle to ~3e-7 relative, and rel_k is
+# a difference of two J's: observed worst 2.3% on the bench batch, tools/flip_diag.py)
+F32_FLIP_MARGIN = 0.25
+F32_MAX_FLIP_FRAC = 1e-3
 
 
 def compare_forward(out, ref, dtype, conv_tol=1e-6, check_gains=True):
     """Compare a SolveOutput with an oracle / golden dict. Returns a report dict:
-    flips (instances whose iteration count differs), worst per-tensor errors over the
-    instances with identical counts, and mismatch counts of the discrete outputs."""
+    flips (instances whose iteration count differs) with the oracle-side decision margins,
+    worst per-tensor errors (X, U, J over every non-failed instance; K, k, J history over the
+    instances with identical counts) and mismatch counts of the discrete outputs."""
     it = as_np(out.iters)
     flips = np.nonzero(it != ref["iters"])[0]
     fail_ref = ref["fail_t"] >= 0
     ok = ~fail_ref & (ref["diverged"] == 0)
     same = ok & (it == ref["iters"])
     rep = {"B": int(it.shape[0]), "flips": flips.tolist(),
-           "flip_margins": [decision_margin(ref, int(i), conv_tol) for i in flips[:32]],
+           "flip_margins": [decision_margin(ref, int(i), conv_tol, min(it[i], ref["iters"][i]) + 1
+                                            if max(it[i], ref["iters"][i]) > min(it[i], ref["iters"][i]) else None)
+                            for i in flips[:64]],
            "fail_mismatch": int(((as_np(out.fail_t) >= 0) != fail_ref).sum()),
            "fail_t_mismatch": int((as_np(out.fail_t)[fail_ref] != ref["fail_t"][fail_ref]).sum()),
            "diverged_mismatch": int((as_np(out.diverged).astype(np.uint8) != ref["diverged"]).sum()),
@@ -82,18 +100,34 @@ def compare_forward(out, ref, dtype, conv_tol=1e-6, check_gains=True):
         b = np.asarray(ref[key])
         if key == "J":
             a, b = a[:, None], b[:, None]
-        e = rel_err(a[same], b[same])
+        # the solution itself is compared on flipped instances too: an extra / missing
+        # iteration at the convergence threshold moves it by less than the tolerance
+        sel = ok if key in ("X", "U", "J") else same
+        e = rel_err(a[sel], b[sel])
         err[key] = float(e.max(initial=0.0))
     rep["err"] = err
     rep["clamp_mismatch"] = int((as_np(out.clamped).astype(np.uint8)[same] != ref["clamped"][same]).any(
         axis=tuple(range(1, ref["clamped"].ndim))).sum())
     rep["converged_mismatch"] = int((as_np(out.converged).astype(np.uint8)[same] != ref["converged"][same]).sum())
-    # the accepted step sizes are discrete: equal after rounding to the kernel's type
+    # the accepted step sizes are discrete: equal after rounding to the kernel's type. An
+    # iteration whose step changed J by no more than conv_tol (relative) on BOTH sides is
+    # a converging no-progress step: "accept a 1e-12 decrease" vs "no step" is round-off
+    # there (candidate costs tie with J), so such mismatches are counted separately.
     ah = as_np(out.alpha_hist).astype(np.float64)
     rh = np.asarray(ref["alpha_hist"], np.float64)
     if dtype == torch.float32:
         rh = rh.astype(np.float32).astype(np.float64)
-    rep["alpha_hist_mismatch"] = int((ah[same] != rh[same]).any(axis=1).sum())
+    mism = np.nonzero(same & (ah != rh).any(axis=1))[0]
+    Jg = as_np(out.J_hist).astype(np.float64)
+    tiny = 0
+    for i in mism:
+        ks = np.nonzero(ah[i] != rh[i])[0] + 1
+        rg = np.abs(Jg[i, ks - 1] - Jg[i, ks]) / np.maximum(1.0, np.abs(Jg[i, ks - 1]))
+        ro = np.abs(ref["J_hist"][i, ks - 1] - ref["J_hist"][i, ks]) / np.maximum(1.0, np.abs(ref["J_hist"][i, ks - 1]))
+        if conv_tol > 0 and np.all(rg <= conv_tol) and np.all(ro <= conv_tol):
+            tiny += 1
+    rep["alpha_hist_mismatch"] = int(len(mism) - tiny)
+    rep["alpha_hist_roundoff"] = int(tiny)
     return rep
 
 
@@ -125,7 +159,12 @@ def assert_forward(rep, dtype, allow_flips=False, xtol=None):
     assert rep["fail_mismatch"] == 0 and rep["fail_t_mismatch"] == 0, rep
     assert rep["diverged_mismatch"] == 0, rep
     if not allow_flips:
-        assert not rep["flips"], f"iteration counts differ at {rep['flips'][:16]} (margins {rep['flip_margins'][:8]})"
+        if dtype == torch.float64:
+            assert not rep["flips"], f"iteration counts differ at {rep['flips'][:16]}"
+        else:
+            assert len(rep["flips"]) <= max(1, F32_MAX_FLIP_FRAC * rep["B"]), f"too many count flips: {rep['flips'][:16]}"
+            bad = [(i, m) for i, m in zip(rep["flips"], rep["flip_margins"]) if not m < F32_FLIP_MARGIN]
+            assert not bad, f"iteration counts differ away from the convergence threshold: {bad[:8]}"
     for key, e in rep["err"].items():
         assert e <= tol, f"{key}: worst rel err {e:.3e} > {tol:g}"
     assert rep["clamp_mismatch"] == 0, f"clamp masks differ on {rep['clamp_mismatch']} instances"

@@ -410,7 +410,6 @@ def test_graphed_update_with_partial_last_minibatch():
     ppo.ppo_update(buf, b2, o2, cfg, solver, generator=torch.Generator().manual_seed(2), graphed=gs)
     for p1, p2 in zip(b1.parameters(), b2.parameters()):
         torch.testing.assert_close(p2, p1, rtol=1e-5, atol=1e-6)
-    assert all(p.grad is v for p, v in zip(gs.reducer.params, gs.reducer.views))
 
 
 @pytest.mark.gpu
