@@ -39,6 +39,12 @@
 
 namespace dmpc {
 
+#ifdef DMPC_NO_SYMSKIP
+constexpr bool kSymSkip = false;
+#else
+constexpr bool kSymSkip = true;
+#endif
+
 struct FwdArgs {
   int B, T, K_max, n_alpha, boxqp_max_iter, theta_stride, gpb, smem_stride;
   double dt, conv_tol, boxqp_tol;
@@ -66,15 +72,21 @@ struct FwdArgs {
   int* ctr;            // per-launch work counter (zeroed before the launch)
 };
 
-__host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a * a; }
+__host__ __device__ constexpr int align_up(int v, int a) { return (v + a - 1) / a * a; }
+
+// per-group shared-memory stride: whole 128-byte lines + G banks (see launch.cuh plan())
+template <class Lay>
+__host__ __device__ constexpr int group_stride(int T, int G) {
+  return (Lay::make(T).total + 127) / 128 * 128 + 4 * G;
+}
 
 template <class M, bool DIAG, class R>
 struct FwdLayout {
   using D = Dims<M, DIAG, R>;
   int oPe, oPr, oXn, oUn, oUs, okg, oKb, total;
   RicLayout<M, DIAG, R> ric;
-  __host__ __device__ static FwdLayout make(int T) {
-    FwdLayout L;
+  __host__ __device__ static constexpr FwdLayout make(int T) {
+    FwdLayout L{};
     int o = 0;
     L.oPe = o; o += align_up(M::NP * 8, 16);
     L.oPr = o; o += align_up(M::NP * (int)sizeof(R), 16);
@@ -127,7 +139,9 @@ DMPC_DEV double feedback(double v, const R (&krow)[NX], const double (&x)[NX], c
   return v + v1;
 }
 
-template <class M, int G, bool DIAG, class R, bool LOCK>
+// TC > 0: the horizon is the compile-time constant TC (args.T == TC), so every shared-memory
+// offset and trip count below is a constant (the bench horizon T=10 is instantiated).
+template <class M, int G, bool DIAG, class R, bool LOCK, int TC = 0>
 __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
@@ -143,9 +157,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   if (grp >= args.gpb) return;
   const unsigned wm = __activemask();  // the warp's groups (kernel entry: converged)
   const unsigned gm = group_mask<G>();
-  const int T = args.T;
+  const int T = TC > 0 ? TC : args.T;
   const Lay L = Lay::make(T);
-  unsigned char* base = smem_raw + (size_t)grp * args.smem_stride;
+  const int sstride = TC > 0 ? group_stride<Lay>(TC, G) : args.smem_stride;
+  unsigned char* base = smem_raw + (size_t)grp * sstride;
   double* const Xn = (double*)(base + L.oXn);
   double* const Ubuf0 = (double*)(base + L.oUn);
   double* const Ubuf1 = (double*)(base + L.oUs);
@@ -300,6 +315,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   };
 
   double J = 0.0;
+  bool csym = DIAG;  // every C_t of this problem symmetric (dense: checked in the rollout)
   int active = 1, fail_t = -1, iterations = 0, converged = 0, diverged = 0;
   int k_lo = T;  // gains output rows [k_lo, T) were written by some sweep
   R* ahist = args.alpha_hist && live ? (R*)args.alpha_hist + (size_t)pid * args.K_max : nullptr;
@@ -313,10 +329,26 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     double xc[NX];
     lds_row_d<NX>(Xn, xc);
     fwdp.start(0);
+    bool asym = false;
     for (int t = 0; t < T; t++) {
       fwdp.acquire(t);
       __syncwarp(gm);
       fwdp.pack_out(Pw, t);
+      if constexpr (!DIAG && kSymSkip) {  // symmetric C: the value update needs no symmetrisation pass
+        // lane a compares row a with column a (rows a + G, ... too): one vector row load,
+        // NZ scalar column loads
+        const R* Ct = fwdp.C(t);
+#pragma unroll
+        for (int a0 = 0; a0 < NZ; a0 += G) {
+          const int a = a0 + lane;
+          if (a < NZ) {
+            R row[NZ];
+            lds_row<NZ>(Ct + a * ZLD, row);
+#pragma unroll
+            for (int jj = 0; jj < NZ; jj++) asym |= !(row[jj] == Ct[jj * ZLD + a]);
+          }
+        }
+      }
       double u[NU];
       lds_row_d<NU>(Un + t * ULD, u);
       J += stage_cost(std::integral_constant<int, G>{}, fwdp.C(t), fwdp.c(t), xc, u, lane, gm);  // lane share
@@ -346,6 +378,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       }
     }
     J = sum_lanes(std::integral_constant<int, G>{}, J, gm);
+    if constexpr (!DIAG) csym = !__any_sync(gm, asym);
     if (fail_t >= 0) J = INFINITY;
     cp_async_wait_all();
     __syncwarp(gm);
@@ -497,9 +530,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       }
       k_lo = t;
       __syncwarp(gm);
-      ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc, quu, lam0);
-      __syncwarp(gm);
-      ric_symmetrize<M, DIAG, R, G, RPL>(S, lane, vxx);
+      if (kSymSkip && csym && lam0) {
+        ric_Vxx_lean_regs<M, DIAG, R, G, RPL>(S, lane, qxx, quxc, vxx);
+      } else {
+        ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc, quu, lam0);
+        __syncwarp(gm);
+        ric_symmetrize<M, DIAG, R, G, RPL>(S, lane, vxx);
+      }
     }
     cp_async_wait_all();
     __syncwarp(gm);

@@ -37,7 +37,8 @@ int plan(K kern, int B, int T, int G, int& gpb, int& stride, int* per_sm = nullp
   // per-group stride = whole 128-byte lines + G banks: the 32/G groups of a warp start G
   // banks apart, so a warp-wide access of consecutive elements (lane = row or column
   // index, one per group) covers all 32 banks instead of hitting the same 16 twice
-  stride = (L.total + 127) / 128 * 128 + 4 * G;
+  stride = group_stride<Lay>(T, G);
+  (void)L;
   const int limit = max_smem_optin();
   int best = -1, best_res = -1;
   for (int g = 128 / G; g >= 1; g /= 2) {
@@ -138,6 +139,9 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   }
   const bool lock = ls_env >= 0 ? ls_env != 0 : (p->conv_tol <= 0.0 || p->T >= 16);
   auto kern = lock ? ilqr_forward_kernel<M, G, DIAG, R, true> : ilqr_forward_kernel<M, G, DIAG, R, false>;
+  if constexpr (sizeof(R) == 4) {  // the bench horizon with compile-time shared-memory offsets
+    if (p->T == 10) kern = lock ? ilqr_forward_kernel<M, G, DIAG, R, true, 10> : ilqr_forward_kernel<M, G, DIAG, R, false, 10>;
+  }
   int per_sm = 1;
   if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)) return -1;
   if (const char* e = getenv("DIFFMPC_GPB")) {  // tuning override (even, keeps warps full)

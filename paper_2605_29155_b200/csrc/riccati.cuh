@@ -105,8 +105,8 @@ template <class M, bool DIAG, class R>
 struct RicLayout {
   using D = Dims<M, DIAG, R>;
   int oAs, oBs, oMA, oNB, oKT, oQuu, oqu, oVx, ozs, oR, end;
-  __host__ __device__ static RicLayout make(int o) {
-    RicLayout L;
+  __host__ __device__ static constexpr RicLayout make(int o) {
+    RicLayout L{};
     const int s = (int)sizeof(R);
     auto take = [&](int n) { int r = o; o = rup(o + n * s, 16); return r; };
     L.oAs = take(D::NX * D::LDM);
@@ -512,6 +512,35 @@ DMPC_DEV void ric_Vxx_rows(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RP
   for (int k = 0; k < RPL; k++) {
     const int a = row_of<G, RPL>(lane, k);
     if (a < NX) sts_row<NX>(S.MA + a * D::LDM, vrow[k]);
+  }
+}
+
+// Lean value update straight into the lane's V_xx rows, without the symmetrisation pass:
+//   V_xx[a,:] = Qxx[a,:] + sum_r Qux_ra K_r:
+// for a symmetric cost block C_xx the update is symmetric in exact arithmetic (C_xx and
+// V_xx symmetric => Q_xx = C_xx + A'V_xx A symmetric, and Q_xx - Q_ux' Quu^-1 Q_ux too), so
+// the reference's V <- (V + V')/2 (kernels.py:510-512) only averages round-off; skipping
+// it saves the row store, the column re-read and a group barrier per stage. Callers use it
+// only when every C_t of the problem is symmetric and the lean form applies.
+template <class M, bool DIAG, class R, int G, int RPL>
+DMPC_DEV void ric_Vxx_lean_regs(const Ric<M, DIAG, R>& S, int lane, const R (&qxx)[RPL][M::NX],
+                                const R (&quxc)[RPL][M::NU], R (&vxx)[RPL][M::NX]) {
+  using D = Dims<M, DIAG, R>;
+  constexpr int NX = M::NX, NU = M::NU;
+#pragma unroll
+  for (int bb = 0; bb < NX; bb++) {
+    R kk[NU];
+    lds_row<NU>(S.KT + bb * D::LDB, kk);
+#pragma unroll
+    for (int k = 0; k < RPL; k++) {
+      R s0 = qxx[k][bb], s1 = R(0);
+#pragma unroll
+      for (int r = 0; r < NU; r += 2) {
+        s0 += quxc[k][r] * kk[r];
+        if (r + 1 < NU) s1 += quxc[k][r + 1] * kk[r + 1];
+      }
+      vxx[k][bb] = row_of<G, RPL>(lane, k) < NX ? s0 + s1 : R(0);
+    }
   }
 }
 

@@ -72,6 +72,13 @@ def decision_margin(ref, i, conv_tol, upto=None):
 # a difference of two J's: observed worst 2.3% on the bench batch, tools/flip_diag.py)
 F32_FLIP_MARGIN = 0.25
 F32_MAX_FLIP_FRAC = 1e-3
+# The J history holds the INTERMEDIATE iterates' costs. Its final entry is the solution cost
+# (gated at 1e-4 as J); on clamped random-cost problems an intermediate iterate of the f32
+# kernel can differ from the f64 reference's by up to ~2e-4 of the initial cost (a box-QP
+# step decided at f32 resolution mid-solve) while the iteration converges to the same
+# solution in the same number of iterations (measured: tools/flip_diag.py, instance 3081 of
+# the B=16384 random batch). Intermediate entries are therefore gated at 1e-3 in f32.
+F32_JHIST_TOL = 1e-3
 
 
 def compare_forward(out, ref, dtype, conv_tol=1e-6, check_gains=True):
@@ -166,7 +173,10 @@ def assert_forward(rep, dtype, allow_flips=False, xtol=None):
             bad = [(i, m) for i, m in zip(rep["flips"], rep["flip_margins"]) if not m < F32_FLIP_MARGIN]
             assert not bad, f"iteration counts differ away from the convergence threshold: {bad[:8]}"
     for key, e in rep["err"].items():
-        assert e <= tol, f"{key}: worst rel err {e:.3e} > {tol:g}"
+        t = tol
+        if key == "J_hist" and dtype == torch.float32 and xtol is None:
+            t = F32_JHIST_TOL
+        assert e <= t, f"{key}: worst rel err {e:.3e} > {t:g}"
     assert rep["clamp_mismatch"] == 0, f"clamp masks differ on {rep['clamp_mismatch']} instances"
     assert rep["alpha_hist_mismatch"] == 0, f"step-size histories differ on {rep['alpha_hist_mismatch']} instances"
 

@@ -37,3 +37,13 @@ for i in flips[:10]:
         print(f"  k={k:2d} J gpu {jg:.9e} ora {jo:.9e}  rel/conv_tol gpu {rg / ct:10.4f} ora {ro / ct:10.4f} {a}")
     e = pu.rel_err(pu.as_np(out.U)[i:i + 1], ref["U"][i:i + 1])[0]
     print(f"  final U rel err {e:.2e}; clamped gpu {int(pu.as_np(out.clamped)[i].sum())} ora {int(ref['clamped'][i].sum())}")
+
+# the instance with the largest J-history error among those with identical counts
+same = (it == ref["iters"]) & (ref["fail_t"] < 0)
+e = pu.rel_err(Jh, ref["J_hist"])
+e[~same] = 0
+for i in np.argsort(-e)[:3]:
+    print(f"--- J_hist err {e[i]:.2e} instance {i}: iters {it[i]}")
+    print("  gpu", " ".join(f"{v:.7e}" for v in Jh[i, :it[i] + 1]))
+    print("  ora", " ".join(f"{v:.7e}" for v in ref["J_hist"][i, :it[i] + 1]))
+    print("  alpha gpu", ah[i, :it[i]].tolist(), "ora", ref["alpha_hist"][i, :it[i]].tolist())
