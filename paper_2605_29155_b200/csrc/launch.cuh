@@ -146,7 +146,7 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)) return -1;
   if (const char* e = getenv("DIFFMPC_GPB")) {  // tuning override (even, keeps warps full)
     const int g = atoi(e);
-    if (g >= 2 && g % 2 == 0 && g * G <= 1024 && g * a.smem_stride <= max_smem_optin()) {
+    if (g >= 2 && g % 2 == 0 && g * G <= 128 && g * a.smem_stride <= max_smem_optin()) {  // launch bounds: 128 threads
       a.gpb = g;
       const int smem_g = g * a.smem_stride;
       if (smem_g > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_g);

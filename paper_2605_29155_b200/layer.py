@@ -3,8 +3,8 @@ signatures and semantics (/root/reference/pkg/src/fusedmpc/policy.py:179-290), r
 the B200 kernels.
 
 Differences a caller can observe, all deliberate:
-  * the solve runs in the input dtype (float32 in training, float64 if diag is float64)
-    on the GPU; the reference always computes in float64 on the CPU (policy.py:235-236);
+  * the solve runs in the solver's dtype on the GPU (MpcSolver(dtype=torch.float32) by
+    default; torch.float64 reproduces the reference's float64 solve, policy.py:235-236);
   * solver state (warm starts, the workspace) stays device-resident as torch tensors;
   * ``pool`` / ``mode`` are accepted for signature compatibility: there is one fused
     kernel per forward solve and one per backward, whatever the mode.
@@ -94,9 +94,10 @@ class MpcSolveLayer(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, diag, cvec, solver, x_init, U_warm, stats_sink):
-        dtype = torch.float64 if diag.dtype == torch.float64 else torch.float32
+        # the solve runs in the solver's precision (MpcSolver(dtype=...): float32 by default,
+        # float64 = the reference's precision, policy.py:235-236); u0 comes back in diag's dtype
         ws, iterations, converged, _, _ = solver.solve_diag(x_init, diag.detach(), cvec.detach(), U_warm,
-                                                            dtype=dtype)
+                                                            dtype=solver.dtype)
         ctx.solver = solver
         ctx.ws = ws
         ctx.out_dtype = diag.dtype

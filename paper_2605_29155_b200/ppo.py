@@ -306,10 +306,11 @@ def ppo_update(buffer: dict, bundle, optimizer, config: TrainConfig, solver=None
             dist.all_reduce(mom, op=dist.ReduceOp.SUM, group=reducer.group if reducer is not None else None)
             N = mom[2]
             mean = mom[0] / N
-            std = torch.sqrt(torch.clamp((mom[1] - N * mean * mean) / (N - 1), min=0.0))
+            std = torch.sqrt(torch.clamp(mom[1] / N - mean * mean, min=0.0))  # population std
             adv = ((buffer["advantages"].to(torch.float64) - mean) / (std + 1e-8)).to(torch.float32)
         else:
-            adv = (adv - adv.mean()) / (adv.std() + 1e-8)
+            # numpy's std (ddof=0) on the float32 advantages, as trainer.py:171-173 computes it
+            adv = (adv - adv.mean()) / (adv.std(correction=0) + 1e-8)
     flat = {"obs": buffer["obs"], "actions": buffer["actions"], "old_log_probs": buffer["log_probs"],
             "advantages": adv, "returns": buffer["returns"].to(torch.float32)}
     if bundle.mode == "ac_mpc":

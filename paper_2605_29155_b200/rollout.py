@@ -24,7 +24,10 @@ class DeviceRollout:
         T, m = bundle.T, bundle.n_u
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
         self.obs = env.reset().to(torch.float32)
-        self.default_u = torch.as_tensor(solver.default_u, dtype=torch.float32, device=self.device)
+        # the solver inputs are kept in the solver's precision (a minibatch re-solve must see
+        # exactly what the rollout solve saw; float64 = the reference's precision)
+        self.sdt = getattr(solver, "dtype", torch.float32)
+        self.default_u = torch.as_tensor(solver.default_u, dtype=self.sdt, device=self.device)
         self.warm = self.default_u.expand(self.N, T, m).clone()
         self.ep_return = torch.zeros(self.N, dtype=torch.float64, device=self.device)
         self.u_lo = torch.as_tensor(bundle.u_min, dtype=torch.float64, device=self.device)
@@ -42,11 +45,17 @@ class DeviceRollout:
         if self.plan is None:  # preallocated launch (the solve's outputs are consumed here)
             from .solver import SolvePlan
             self.plan = SolvePlan(self.solver.model, self.solver.settings, self.N, layout="diag",
-                                  dtype=torch.float32, device=self.device, want_gains=False, backward=False,
+                                  dtype=self.sdt, device=self.device, want_gains=False, backward=False,
                                   kernel=getattr(self.solver, "kernel", "throughput"))
-        ws = self.plan.solve(x_init.to(torch.float32).contiguous(), diag.contiguous(), cvec.contiguous(), U_warm)
+        ws = self.plan.solve(x_init.to(self.sdt).contiguous(), diag.to(self.sdt).contiguous(),
+                             cvec.to(self.sdt).contiguous(), U_warm)
         self.warm = torch.cat([ws.U[:, 1:], ws.U[:, -1:]], dim=1)
-        return ws.U[:, 0].clone(), x_init, U_warm, ws.iters.clone()
+        return ws.U[:, 0].to(torch.float32, copy=True), x_init, U_warm, ws.iters.clone()  # float32 means (trainer.py:273)
+
+    def noise(self, step, shape):
+        """Standard-normal exploration noise of one step (trainer.py:283: one (N, m) draw per
+        step from the rollout's generator). Tests substitute the reference's draws."""
+        return torch.randn(shape, generator=self.gen, dtype=torch.float32, device=self.device)
 
     # state carried from one collection to the next (rollout + environment)
     _STATE = ("obs", "warm", "ep_return")
@@ -115,7 +124,8 @@ class DeviceRollout:
                "log_probs": torch.empty((S, N), **f32), "values": torch.empty((S, N), dtype=torch.float64, device=dev),
                "rewards": torch.empty((S, N), dtype=torch.float64, device=dev),
                "dones": torch.empty((S, N), dtype=torch.float64, device=dev),
-               "x_init": torch.empty((S, N, b.n_x), **f32), "U_warm": torch.empty((S, N, b.T, b.n_u), **f32)}
+               "x_init": torch.empty((S, N, b.n_x), dtype=self.sdt, device=dev),
+               "U_warm": torch.empty((S, N, b.T, b.n_u), dtype=self.sdt, device=dev)}
         sigma = torch.exp(b.log_sigma.detach())
         ep_sum = torch.zeros((), dtype=torch.float64, device=dev)
         ep_cnt = torch.zeros((), dtype=torch.int64, device=dev)
@@ -125,7 +135,7 @@ class DeviceRollout:
             u_mean, x_init, U_warm, it = self.policy_means(self.obs)
             iters += it.sum()
             values = b.critic(self.obs).to(torch.float64)
-            eps = torch.randn(u_mean.shape, generator=self.gen, **f32)
+            eps = self.noise(s, u_mean.shape)
             actions = u_mean + sigma * eps
             log_probs = torch.distributions.Normal(u_mean, sigma, validate_args=False).log_prob(actions).sum(-1)
             u_exec = torch.clamp(actions.to(torch.float64), self.u_lo, self.u_hi)
@@ -133,7 +143,7 @@ class DeviceRollout:
             buf["actions"][s] = actions
             buf["log_probs"][s] = log_probs
             buf["values"][s] = values
-            buf["x_init"][s] = x_init.to(torch.float32)
+            buf["x_init"][s] = x_init.to(self.sdt)
             buf["U_warm"][s] = U_warm
             _, reward, done, reason = self.env.step(u_exec)
             buf["rewards"][s] = reward

@@ -146,7 +146,7 @@ def test_data_parallel_update_on_rank_local_buffers():
     opt = torch.optim.Adam(b.parameters(), lr=1e-3)
     bufs = [_buffer(96, model, st.T, seed=10 + r) for r in range(2)]
     adv = torch.cat([x["advantages"] for x in bufs])
-    mean, std = adv.mean(), adv.std()
+    mean, std = adv.mean(), adv.std(correction=0)
     gen = torch.Generator().manual_seed(3)
     for _ in range(cfg.sgd_epochs):
         perm = torch.randperm(96, generator=gen)
