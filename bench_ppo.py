@@ -34,8 +34,11 @@ def main():
     ap.add_argument("--T", type=int, default=10)
     ap.add_argument("--mode", default="update", choices=["update", "train"],
                     help="update: PPO minibatch steps (13-state quadrotor); train: full device-resident "
-                         "PPO iterations (batched race env rollout collection + update, planar model)")
+                         "PPO iterations (batched race env rollout collection + update)")
     ap.add_argument("--envs", type=int, default=1024, help="train mode: environments per GPU")
+    ap.add_argument("--model", default="quad13", choices=["quad13", "planar"],
+                    help="train mode: 13-state quadrotor on the 3-D helix5 track (BASELINE model) or the "
+                         "reference's planar quadrotor on hairpin5")
     ap.add_argument("--rollout-steps", type=int, default=32, help="train mode: steps per update")
     ap.add_argument("--no-graph", action="store_true",
                     help="update mode: eager minibatch steps (default: one CUDA graph per step when "
@@ -157,11 +160,17 @@ def train_mode(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("gloo" if share else "nccl", **({} if share else {"device_id": dev}))
-    model = DynModel.planar_quadrotor(dt=0.05)
-    st = SolveSettings(T=args.T, u_min=0.0, u_max=2 * 0.5 * 9.81)
+    if args.model == "quad13":
+        model = DynModel.quadrotor(dt=0.05)
+        st = SolveSettings(T=args.T, u_min=0.0, u_max=float(model.mass * model.gravity))
+        track, obs_dim = raceenv.helix5(), raceenv.OBS_DIM_3D
+    else:
+        model = DynModel.planar_quadrotor(dt=0.05)
+        st = SolveSettings(T=args.T, u_min=0.0, u_max=2 * 0.5 * 9.81)
+        track, obs_dim = raceenv.hairpin5(), raceenv.OBS_DIM
     torch.manual_seed(0)
-    bundle = PolicyBundle("ac_mpc", raceenv.OBS_DIM, model, st, CostHeadScaling.for_model(model, 6)).to(dev)
-    env = raceenv.BatchedRaceEnv(raceenv.hairpin5(), model, args.envs, device=dev, seed=11 + rank)
+    bundle = PolicyBundle("ac_mpc", obs_dim, model, st, CostHeadScaling.for_model(model, model.n_x)).to(dev)
+    env = raceenv.BatchedRaceEnv(track, model, args.envs, device=dev, seed=11 + rank)
     solver = MpcSolver(model, st, device=dev)
     cfg = ppo.TrainConfig(steps_per_update=args.rollout_steps, minibatch_size=args.minibatch, sgd_epochs=1)
     opt = torch.optim.Adam(bundle.parameters(), lr=cfg.lr_start)
@@ -211,12 +220,14 @@ def train_mode(args):
     if rank == 0:
         samples = args.envs * args.rollout_steps
         print(json.dumps({
-            "metric": "AC-MPC PPO iterations/s (device-resident rollout + update, planar race env)",
+            "metric": f"AC-MPC PPO iterations/s (device-resident rollout + update, {args.model} race env)",
             "value": 1e3 / ms, "unit": "iterations/s", "env_steps_per_s": world * samples * 1e3 / ms,
             "n_gpus": world, "iterations": K, "ms_per_iteration": ms, "higher_is_better": True,
             "scaling": "weak", "dtype": "f32", "data": "synthetic (race env, random-init policy)",
-            "config": {"workload": "PPO: collect envs x steps with one DiffMPC forward per step, GAE, "
-                                   "1 epoch of minibatch updates", "T": args.T, "envs_per_gpu": args.envs,
+            "config": {"workload": "PPO: collect envs x steps with one DiffMPC forward and one fused env-step "
+                                   "kernel per step, GAE, 1 epoch of minibatch updates", "model": args.model,
+                       "track": "helix5 (3-D)" if args.model == "quad13" else "hairpin5", "T": args.T,
+                       "envs_per_gpu": args.envs,
                        "rollout_steps": args.rollout_steps, "minibatch_per_gpu": args.minibatch // world,
                        "parallelism": f"dp{world}"},
             "diffmpc_launches_per_iteration": (_lib.launch_count() - l0) / K,

@@ -157,6 +157,41 @@ int diffmpc_dynamics_f32(const DiffMPCProblem* p, int32_t N, const void* theta, 
 int diffmpc_dynamics_f64(const DiffMPCProblem* p, int32_t N, const void* theta, const void* x,
                          const void* u, void* xn, void* A, void* Bm, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Batched gate-racing environment step (the AC-MPC training environment, SURVEY.md §8(f)
+ * row 3). Replaces, per environment, raceenv.env_step + raceenv.observation
+ * (/root/reference/pkg/src/fusedmpc/raceenv.py:120-140, 174-228) for N environments in ONE
+ * kernel launch; planar quadrotor on a 2-D track (dim 2, the reference's environment) or the
+ * 13-state quadrotor on a 3-D track (dim 3: circular gate openings, 19-value observation).
+ * ------------------------------------------------------------------------------------- */
+#define DIFFMPC_RACE_MAX_GATES 32
+#define DIFFMPC_RACE_NONE           0
+#define DIFFMPC_RACE_LAP_COMPLETE   1
+#define DIFFMPC_RACE_GATE_MISSED    2
+#define DIFFMPC_RACE_OUT_OF_BOUNDS  3
+#define DIFFMPC_RACE_TIMEOUT        4
+
+typedef struct DiffMPCTrack {
+  int32_t n_gates, laps, dim;                 /* dim 2 (planar) or 3                     */
+  int32_t pad_;
+  double center[DIFFMPC_RACE_MAX_GATES][3];   /* gate centres (first `dim` entries)       */
+  double normal[DIFFMPC_RACE_MAX_GATES][3];   /* unit normals (passing direction)         */
+  double width[DIFFMPC_RACE_MAX_GATES];       /* opening width (3-D: diameter)            */
+  double lo[3], hi[3];                        /* in-bounds box of the position            */
+  /* RewardConfig (raceenv.py:88-99) and the observation scales (raceenv.py:30-32)        */
+  double k_p, gate_bonus, crash_penalty, time_penalty, progress_cap, timeout, miss_factor;
+  double pos_scale, vel_scale, omega_scale;
+} DiffMPCTrack;
+
+/* Advances every environment that is not done by one control period with controls u (N,nu)
+ * (already clamped by the caller): x (N,nx), gate / laps / reason (N) int64, t (N), done (N)
+ * uint8 are updated in place; reward (N) is written (0 for environments already done);
+ * obs (N, 11 | 19) receives the next observation (NULL: skipped). Device pointers, float64. */
+int diffmpc_race_step_f64(const DiffMPCTrack* track, int32_t model_kind, int32_t N, double dt,
+                          const double* theta, double* x, int64_t* gate, int64_t* laps, double* t,
+                          uint8_t* done, int64_t* reason, const double* u, double* reward, double* obs,
+                          void* stream);
+
 /* Bytes of device workspace one forward call needs (elem_bytes 4 for _f32, 8 for _f64):
  * a work counter for the persistent grid plus the L2-resident feedback gains. This is the
  * counterpart of the reference's preallocated Workspace gains arrays (ilqr.py:84-113). */

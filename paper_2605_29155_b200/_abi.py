@@ -65,6 +65,38 @@ class DiffMPCBackwardIO(ctypes.Structure):
         "dX", "dU", "fail_t")]
 
 
+RACE_MAX_GATES = 32
+
+
+class DiffMPCTrack(ctypes.Structure):
+    """include/diffmpc.h DiffMPCTrack (the batched race-environment step)."""
+    _fields_ = [
+        ("n_gates", ctypes.c_int32), ("laps", ctypes.c_int32), ("dim", ctypes.c_int32), ("pad_", ctypes.c_int32),
+        ("center", (ctypes.c_double * 3) * RACE_MAX_GATES), ("normal", (ctypes.c_double * 3) * RACE_MAX_GATES),
+        ("width", ctypes.c_double * RACE_MAX_GATES), ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
+    ] + [(n, ctypes.c_double) for n in ("k_p", "gate_bonus", "crash_penalty", "time_penalty", "progress_cap",
+                                         "timeout", "miss_factor", "pos_scale", "vel_scale", "omega_scale")]
+
+
+def make_track(track, cfg, pos_scale, vel_scale, omega_scale) -> DiffMPCTrack:
+    G = len(track.gates)
+    if G > RACE_MAX_GATES:
+        raise ConfigError(f"at most {RACE_MAX_GATES} gates are supported")
+    t = DiffMPCTrack()
+    t.n_gates, t.laps, t.dim = G, int(track.laps), int(track.dim)
+    for i, g in enumerate(track.gates):
+        for a in range(track.dim):
+            t.center[i][a] = float(g.center[a])
+            t.normal[i][a] = float(g.normal[a])
+        t.width[i] = float(g.width)
+    for a in range(track.dim):
+        t.lo[a], t.hi[a] = float(track.lo[a]), float(track.hi[a])
+    for n in ("k_p", "gate_bonus", "crash_penalty", "time_penalty", "progress_cap", "timeout", "miss_factor"):
+        setattr(t, n, float(getattr(cfg, n)))
+    t.pos_scale, t.vel_scale, t.omega_scale = float(pos_scale), float(vel_scale), float(omega_scale)
+    return t
+
+
 def make_problem(model, settings, B: int, layout: int, theta_stride: int = 0, kernel="auto") -> DiffMPCProblem:
     """Fill a DiffMPCProblem from the reference-style model/settings objects."""
     nu = model.n_u

@@ -24,7 +24,7 @@ _lib = None
 EXPORTS = (
     "diffmpc_forward_f32", "diffmpc_forward_f64", "diffmpc_backward_f32", "diffmpc_backward_f64",
     "diffmpc_dynamics_f32", "diffmpc_dynamics_f64", "diffmpc_supported", "diffmpc_launch_count",
-    "diffmpc_last_error", "diffmpc_abi_version",
+    "diffmpc_last_error", "diffmpc_abi_version", "diffmpc_race_step_f64",
 )
 
 
@@ -51,6 +51,8 @@ def lib():
             f = getattr(L, f"diffmpc_dynamics_{dt}")
             f.argtypes = [vp, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp]
             f.restype = ctypes.c_int
+        L.diffmpc_race_step_f64.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double] + [vp] * 11
+        L.diffmpc_race_step_f64.restype = ctypes.c_int
         L.diffmpc_forward_workspace_bytes.argtypes = [vp, ctypes.c_int32]
         L.diffmpc_forward_workspace_bytes.restype = ctypes.c_uint64
         L.diffmpc_supported.argtypes = [ctypes.c_int32] * 3

@@ -1,21 +1,26 @@
-"""Batched planar gate-racing environment, stepped on the GPU.
+"""Batched gate-racing environments, stepped on the GPU.
 
-Semantics follow /root/reference/pkg/src/fusedmpc/raceenv.py per environment: gates are
+Planar (the reference's environment, /root/reference/pkg/src/fusedmpc/raceenv.py): gates are
 segments of a given width centred on ``center`` and perpendicular to the unit ``normal``;
-passing = crossing the gate plane in the normal direction within half a width of the
-centre (boundary inclusive); crossing within ``miss_factor`` half-widths is a terminal
-miss; shaped progress reward toward the next gate, gate bonus, crash / time penalties,
-timeout (raceenv.py:174-228). The observation (11 values, raceenv.py:120-140) and the
-MPC state (drone state translated to the next gate, raceenv.py:143-149) are the
-reference's.
+passing = crossing the gate plane in the normal direction within half a width of the centre
+(boundary inclusive); crossing within ``miss_factor`` half-widths is a terminal miss; shaped
+progress reward toward the next gate, gate bonus, crash / time penalties, timeout
+(raceenv.py:174-228). Observation: 11 values (raceenv.py:120-140); MPC state: the drone
+state translated so the next gate's centre is the origin (raceenv.py:143-149).
 
-B200 design: the N environments live in device tensors (state (N,6) float64, gate index,
-lap count, episode time, done flags); one ``step`` advances all of them with the drone
-dynamics evaluated by the library's CUDA dynamics kernel (``diffmpc_dynamics_f64``, the
-same model code the iLQR kernels use) and the gate / reward logic as batched tensor ops —
-no host round trip, so rollout collection stays on the device. Random spawn perturbations
-come from a device ``torch.Generator`` (the reference draws per-env numpy streams; the
-distributions match, the streams do not).
+3-D (new; the 13-state quadrotor of BASELINE config 4, which the reference does not have):
+the same rules with circular gate openings of diameter ``width`` (a crossing passes when the
+crossing point lies within width/2 of the centre in the gate plane) and a 19-value
+observation: [(g1 - p) * POS_SCALE (3), n1 (3), (g2 - p) * POS_SCALE (3), v * VEL_SCALE (3),
+q (4, w x y z), omega * OMEGA_SCALE (3)].
+
+B200 design: the N environments live in device tensors (state (N,nx) float64, gate index,
+lap count, episode time, done flags) and ``step`` is ONE kernel launch
+(``diffmpc_race_step_f64``, csrc/raceenv.cu: dynamics with the library's model code, gate
+logic, reward, termination and the next observation per thread) — no host round trip, so
+rollout collection stays on the device and is capturable in a CUDA graph. Random spawn
+perturbations come from a device ``torch.Generator`` (the reference draws per-env numpy
+streams; the distributions match, the streams do not).
 """
 
 from __future__ import annotations
@@ -28,7 +33,8 @@ import torch
 from .dynamics import DynModel
 from .errors import ConfigError
 
-OBS_DIM = 11
+OBS_DIM = 11       # planar observation (raceenv.py:120-140)
+OBS_DIM_3D = 19    # 3-D observation (13-state quadrotor), see the module docstring
 POS_SCALE = 0.2
 VEL_SCALE = 0.2
 OMEGA_SCALE = 0.2
@@ -68,7 +74,11 @@ class TrackSpec:
             raise ConfigError("a track needs at least 2 gates")
         if self.laps < 1:
             raise ConfigError("laps must be >= 1")
-        pts = np.array([g.center for g in self.gates] + [self.spawn[:2]])
+        dims = {len(g.center) for g in self.gates} | {len(g.normal) for g in self.gates}
+        if len(dims) != 1 or dims.pop() not in (2, 3):
+            raise ConfigError("gate centres and normals must all be 2-D (planar) or all 3-D")
+        object.__setattr__(self, "dim", len(self.gates[0].center))
+        pts = np.array([g.center for g in self.gates] + [self.spawn[:self.dim]])
         object.__setattr__(self, "lo", pts.min(axis=0) - self.margin)
         object.__setattr__(self, "hi", pts.max(axis=0) + self.margin)
 
@@ -94,6 +104,22 @@ def hairpin5() -> TrackSpec:
     return TrackSpec(gates=[Gate(np.array(c), np.array(n), 3.0) for c, n in g], laps=1, spawn=np.zeros(6))
 
 
+def helix5() -> TrackSpec:
+    """A 3-D counterpart of hairpin5 for the 13-state quadrotor: five 1.5 m-diameter gates on
+    a climbing then descending loop, passed counter-clockwise; spawn at rest (hover
+    attitude) 1 m above the ground level of the first gate."""
+    gates = []
+    for k in range(5):
+        a = 2.0 * np.pi * k / 5.0
+        c = np.array([6.0 * np.cos(a), 6.0 * np.sin(a), 2.0 + 1.0 * np.sin(a)])
+        tang = np.array([-np.sin(a), np.cos(a), 1.0 * np.cos(a) / 6.0])  # d(c)/da, normalised
+        gates.append(Gate(c, tang / np.linalg.norm(tang), 1.5))
+    spawn = np.zeros(13)
+    spawn[0:3] = [6.0, -3.0, 1.0]
+    spawn[3] = 1.0
+    return TrackSpec(gates=gates, laps=1, spawn=spawn)
+
+
 @dataclass(frozen=True)
 class RewardConfig:
     """raceenv.py:88-99 (same defaults)."""
@@ -108,49 +134,63 @@ class RewardConfig:
 
 
 class BatchedRaceEnv:
-    """N environments on one device; ``step`` advances all of them at once."""
+    """N environments on one device; ``step`` advances all of them in one kernel launch.
+    Planar quadrotor (6 states, 2 rotors) on a 2-D track, or the 13-state quadrotor on a 3-D
+    track (e.g. ``helix5()``)."""
 
     def __init__(self, track: TrackSpec, model: DynModel, n_envs: int, cfg: RewardConfig = RewardConfig(),
                  device=None, seed: int = 0, reset_noise: float = 0.1):
-        if model.n_x != 6 or model.n_u != 2:
-            raise ConfigError("the race environment is planar (6 states, 2 rotors)")
+        from . import _abi
+        from .dynamics import KIND_PLANAR_QUADROTOR, KIND_QUADROTOR13
+
+        if track.dim == 2 and model.kind == KIND_PLANAR_QUADROTOR:
+            self.pos, self.vel, self.obs_dim = slice(0, 2), slice(3, 5), OBS_DIM
+        elif track.dim == 3 and model.kind == KIND_QUADROTOR13:
+            self.pos, self.vel, self.obs_dim = slice(0, 3), slice(7, 10), OBS_DIM_3D
+        else:
+            raise ConfigError("race environments: planar quadrotor on a 2-D track or the 13-state "
+                              "quadrotor on a 3-D track")
+        if len(track.spawn) != model.n_x:
+            raise ConfigError(f"spawn state must have {model.n_x} entries")
         self.track, self.model, self.cfg, self.N = track, model, cfg, int(n_envs)
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.reset_noise = float(reset_noise)
+        self.D = track.dim
         f = dict(dtype=torch.float64, device=self.device)
         self.centers = torch.tensor(np.stack([g.center for g in track.gates]), **f)
         self.normals = torch.tensor(np.stack([g.normal for g in track.gates]), **f)
-        self.widths = torch.tensor([g.width for g in track.gates], **f)
-        self.lo = torch.tensor(track.lo, **f)
-        self.hi = torch.tensor(track.hi, **f)
         self.spawn = torch.tensor(track.spawn, **f)
+        self.theta = torch.tensor(np.asarray(model.params, dtype=np.float64), **f)
         self.n_gates = len(track.gates)
+        self._track = _abi.make_track(track, cfg, POS_SCALE, VEL_SCALE, OMEGA_SCALE)
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
-        self.x = self.spawn.expand(self.N, 6).clone()
+        self.x = self.spawn.expand(self.N, model.n_x).clone()
         self.gate = torch.zeros(self.N, dtype=torch.int64, device=self.device)
         self.laps = torch.zeros_like(self.gate)
         self.t = torch.zeros(self.N, **f)
         self.done = torch.zeros(self.N, dtype=torch.bool, device=self.device)
         self.reason = torch.zeros(self.N, dtype=torch.int64, device=self.device)
-        self.obs_dim = OBS_DIM
 
     # --------------------------------------------------------------- queries
     def observation(self) -> torch.Tensor:
-        """(N, 11) float64 (raceenv.py:120-140)."""
-        x = self.x
+        """(N, 11) planar (raceenv.py:120-140) or (N, 19) 3-D observation, float64."""
+        x, D = self.x, self.D
         g1 = self.gate
-        g2 = (g1 + 1) % self.n_gates
-        c1, n1, c2 = self.centers[g1], self.normals[g1], self.centers[g2]
-        return torch.stack([
-            (c1[:, 0] - x[:, 0]) * POS_SCALE, (c1[:, 1] - x[:, 1]) * POS_SCALE, n1[:, 0], n1[:, 1],
-            (c2[:, 0] - x[:, 0]) * POS_SCALE, (c2[:, 1] - x[:, 1]) * POS_SCALE,
-            x[:, 3] * VEL_SCALE, x[:, 4] * VEL_SCALE, torch.sin(x[:, 2]), torch.cos(x[:, 2]),
-            x[:, 5] * OMEGA_SCALE], dim=1)
+        c1, n1, c2 = self.centers[g1], self.normals[g1], self.centers[(g1 + 1) % self.n_gates]
+        p = x[:, self.pos]
+        if D == 2:
+            return torch.stack([
+                (c1[:, 0] - p[:, 0]) * POS_SCALE, (c1[:, 1] - p[:, 1]) * POS_SCALE, n1[:, 0], n1[:, 1],
+                (c2[:, 0] - p[:, 0]) * POS_SCALE, (c2[:, 1] - p[:, 1]) * POS_SCALE,
+                x[:, 3] * VEL_SCALE, x[:, 4] * VEL_SCALE, torch.sin(x[:, 2]), torch.cos(x[:, 2]),
+                x[:, 5] * OMEGA_SCALE], dim=1)
+        return torch.cat([(c1 - p) * POS_SCALE, n1, (c2 - p) * POS_SCALE, x[:, self.vel] * VEL_SCALE,
+                          x[:, 3:7], x[:, 10:13] * OMEGA_SCALE], dim=1)
 
     def mpc_state(self) -> torch.Tensor:
         """Drone state translated so the next gate centre is the origin (raceenv.py:143-149)."""
         x = self.x.clone()
-        x[:, 0:2] -= self.centers[self.gate]
+        x[:, self.pos] -= self.centers[self.gate]
         return x
 
     # --------------------------------------------------------------- dynamics
@@ -158,12 +198,11 @@ class BatchedRaceEnv:
         """Respawn the masked environments (all if None) with the Gaussian position
         perturbation of raceenv.py:152-158; returns the full observation."""
         m = torch.ones(self.N, dtype=torch.bool, device=self.device) if mask is None else mask
-        x = self.spawn.expand(self.N, 6).clone()
+        x = self.spawn.expand(self.N, self.model.n_x).clone()
         if self.reset_noise > 0.0:
-            x[:, 0:2] += self.reset_noise * torch.randn((self.N, 2), generator=self.gen, dtype=torch.float64,
-                                                        device=self.device)
-        mm = m[:, None]
-        self.x = torch.where(mm, x, self.x)
+            x[:, self.pos] += self.reset_noise * torch.randn((self.N, self.D), generator=self.gen,
+                                                             dtype=torch.float64, device=self.device)
+        self.x = torch.where(m[:, None], x, self.x)
         self.gate = torch.where(m, 0, self.gate)
         self.laps = torch.where(m, 0, self.laps)
         self.t = torch.where(m, 0.0, self.t)
@@ -172,60 +211,27 @@ class BatchedRaceEnv:
         return self.observation()
 
     def step(self, u: torch.Tensor):
-        """Advance every environment one control period (raceenv.py:174-228).
+        """Advance every environment one control period (raceenv.py:174-228) in ONE kernel.
 
-        Returns (obs (N,11), reward (N,), done (N,), reason (N,)); environments that were
-        already done are not advanced (the reference raises; callers reset them)."""
-        from .solver import dynamics_t
+        Returns (obs (N, obs_dim), reward (N,), done (N,), reason (N,)); environments that
+        were already done are not advanced (the reference raises; callers reset them)."""
+        import ctypes
 
-        cfg = self.cfg
-        live = ~self.done
-        u = u.to(device=self.device, dtype=torch.float64)
-        x_new, _, _ = dynamics_t(self.model, self.x, u, dtype=torch.float64, device=self.device)
-        t_new = self.t + self.model.dt
-        gi = self.gate
-        c, n, w = self.centers[gi], self.normals[gi], self.widths[gi]
-        p_prev, p_new = self.x[:, 0:2], x_new[:, 0:2]
-        reward = torch.full((self.N,), -cfg.time_penalty * self.model.dt, dtype=torch.float64, device=self.device)
-        finite = torch.isfinite(x_new).all(dim=1)
-        x_new = torch.where(torch.isfinite(x_new), x_new, torch.zeros_like(x_new))
-        # shaped progress
-        d_prev = torch.linalg.vector_norm(p_prev - c, dim=1)
-        d_new = torch.linalg.vector_norm(p_new - c, dim=1)
-        reward = reward + torch.where(finite, torch.clamp(cfg.k_p * (d_prev - d_new), -cfg.progress_cap,
-                                                          cfg.progress_cap), 0.0)
-        # gate-plane crossing (raceenv.py:161-171)
-        s_prev = ((p_prev - c) * n).sum(1)
-        s_new = ((p_new - c) * n).sum(1)
-        crossed = (s_prev <= 0.0) & (s_new > 0.0)
-        denom = s_prev - s_new
-        frac = torch.where(s_new != s_prev, s_prev / torch.where(denom == 0, 1.0, denom), 0.0)
-        p_cross = p_prev + frac[:, None] * (p_new - p_prev)
-        tang = torch.stack([-n[:, 1], n[:, 0]], dim=1)
-        lateral = ((p_cross - c) * tang).sum(1).abs()
-        hw = w / 2.0
-        passed = finite & crossed & (lateral <= hw)
-        missed = finite & crossed & ~passed & (lateral <= cfg.miss_factor * hw)
-        inb = ((p_new >= self.lo) & (p_new <= self.hi)).all(dim=1)
-        oob = ~finite | (finite & ~passed & ~missed & ~inb)
-        reward = reward + torch.where(passed, cfg.gate_bonus, 0.0)
-        nxt = self.gate + passed.to(torch.int64)
-        wrap = nxt == self.n_gates
-        laps = self.laps + wrap.to(torch.int64)
-        nxt = torch.where(wrap, 0, nxt)
-        lap_done = wrap & (laps >= self.track.laps)
-        reward = reward - torch.where(missed | oob, cfg.crash_penalty, 0.0)
-        done = lap_done | missed | oob
-        timeout = ~done & (t_new >= cfg.timeout)
-        done = done | timeout
-        reason = torch.where(lap_done, REASON_LAP, torch.where(missed, REASON_MISS, torch.where(
-            oob, REASON_OOB, torch.where(timeout, REASON_TIMEOUT, REASON_NONE))))
-        # only live environments advance
-        self.x = torch.where(live[:, None], x_new, self.x)
-        self.t = torch.where(live, t_new, self.t)
-        self.gate = torch.where(live, nxt, self.gate)
-        self.laps = torch.where(live, laps, self.laps)
-        self.reason = torch.where(live, reason, self.reason)
-        reward = torch.where(live, reward, 0.0)
-        self.done = self.done | (live & done)
-        return self.observation(), reward, self.done.clone(), self.reason.clone()
+        from . import _lib
+        from .solver import _stream
+
+        u = u.to(device=self.device, dtype=torch.float64).contiguous()
+        if tuple(u.shape) != (self.N, self.model.n_u):
+            raise ConfigError(f"u must be ({self.N}, {self.model.n_u})")
+        for name in ("x", "gate", "laps", "t", "done", "reason"):
+            v = getattr(self, name)
+            if not v.is_contiguous():
+                setattr(self, name, v.contiguous())
+        reward = torch.empty(self.N, dtype=torch.float64, device=self.device)
+        obs = torch.empty((self.N, self.obs_dim), dtype=torch.float64, device=self.device)
+        P = lambda t: t.data_ptr()  # noqa: E731
+        _lib.check(_lib.lib().diffmpc_race_step_f64(
+            ctypes.byref(self._track), int(self.model.kind), self.N, float(self.model.dt), P(self.theta),
+            P(self.x), P(self.gate), P(self.laps), P(self.t), P(self.done), P(self.reason), P(u), P(reward), P(obs),
+            _stream(None, self.device)))
+        return obs, reward, self.done.clone(), self.reason.clone()

@@ -16,7 +16,7 @@ from paper_2605_29155_b200.settings import SolveSettings
 GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 SOLVE_CASES = sorted(
     os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
-    if os.path.basename(p) not in ("boxqp.npz", "dynamics.npz", "raceenv.npz")
+    if os.path.basename(p) not in ("boxqp.npz", "dynamics.npz", "raceenv.npz", "ppo.npz")
 )
 
 

@@ -49,9 +49,10 @@ def test_struct_layout_matches_header():
 #include <stddef.h>
 #include "diffmpc.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(DiffMPCProblem), offsetof(DiffMPCProblem, dt),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(DiffMPCProblem), offsetof(DiffMPCProblem, dt),
          offsetof(DiffMPCProblem, u_min), offsetof(DiffMPCProblem, alphas), sizeof(DiffMPCForwardIO),
-         sizeof(DiffMPCBackwardIO), offsetof(DiffMPCBackwardIO, fail_t));
+         sizeof(DiffMPCBackwardIO), offsetof(DiffMPCBackwardIO, fail_t), sizeof(DiffMPCTrack),
+         offsetof(DiffMPCTrack, width), offsetof(DiffMPCTrack, k_p), offsetof(DiffMPCTrack, omega_scale));
   return 0;
 }
 '''
@@ -61,9 +62,10 @@ int main(void) {
     exe = os.path.join(d, "l")
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
     got = [int(v) for v in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
-    P, F, Bk = _abi.DiffMPCProblem, _abi.DiffMPCForwardIO, _abi.DiffMPCBackwardIO
+    P, F, Bk, Tr = _abi.DiffMPCProblem, _abi.DiffMPCForwardIO, _abi.DiffMPCBackwardIO, _abi.DiffMPCTrack
     want = [ctypes.sizeof(P), P.dt.offset, P.u_min.offset, P.alphas.offset, ctypes.sizeof(F),
-            ctypes.sizeof(Bk), Bk.fail_t.offset]
+            ctypes.sizeof(Bk), Bk.fail_t.offset, ctypes.sizeof(Tr), Tr.width.offset, Tr.k_p.offset,
+            Tr.omega_scale.offset]
     assert got == want
 
 
