@@ -257,6 +257,37 @@ DMPC_DEV int boxqp(const T (&H)[NU][NU], T lam, const T (&g)[NU], const T (&lo)[
   return 0;
 }
 
+// The interior fast path of stage_qp (below), straight-line: every quantity is computed
+// unconditionally and the validity is returned (true iff stage_qp would take its fast path;
+// du / fr / ch are then exactly what stage_qp returns). Used where the QP sits alone on a
+// latency-critical path (the block-per-problem kernel): no branches until the caller's
+// single "fall back to stage_qp" test.
+template <int NU, class T>
+DMPC_DEV bool qp_interior(const T (&Quu)[NU][NU], const T (&qu)[NU], const T (&lo)[NU], const T (&hi)[NU],
+                          T tol, T (&du)[NU], bool (&fr)[NU], Chol<NU, T>& ch) {
+  bool inside = true, all_free[NU];
+  T gn = T(0);
+#pragma unroll
+  for (int a = 0; a < NU; a++) {
+    inside = inside && (lo[a] < T(0)) && (hi[a] > T(0));
+    all_free[a] = true;
+    gn += qu[a] * qu[a];
+  }
+  const bool pd = chol_masked<NU, T>(Quu, T(0), all_free, ch);
+  T sol[NU];
+  chol_solve<NU, T>(ch, qu, sol);
+  bool strict = true;
+  T sdotg = T(0);
+#pragma unroll
+  for (int a = 0; a < NU; a++) {
+    strict = strict && (-sol[a] > lo[a]) && (-sol[a] < hi[a]);
+    sdotg -= sol[a] * qu[a];
+    du[a] = -sol[a];
+    fr[a] = true;
+  }
+  return inside && pd && strict && sdotg < T(0) && !(sqrt_(gn) <= tol);
+}
+
 // The lambda-regularised stage solve of backward_range (kernels.py:440-471).
 // On success: du (the feedforward k_t), fr (free mask), ch (Cholesky of the
 // regularised free block, used for the K columns). The lambda schedule is

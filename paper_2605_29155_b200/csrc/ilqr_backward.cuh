@@ -43,8 +43,8 @@ struct BwdLayout {
   using D = Dims<M, DIAG, R>;
   int oPr, oX, oU, oK, ok, odX, odU, ocl, olam, olh, total;
   RicLayout<M, DIAG, R> ric;
-  __host__ __device__ static BwdLayout make(int T) {
-    BwdLayout L;
+  __host__ __device__ static constexpr BwdLayout make(int T) {
+    BwdLayout L{};
     const int s = (int)sizeof(R);
     int o = 0;
     auto take = [&](int bytes) { int r = o; o = align_up(o + bytes, 16); return r; };
@@ -64,7 +64,8 @@ struct BwdLayout {
   }
 };
 
-template <class M, int G, bool DIAG, class R>
+// TC > 0: compile-time horizon (args.T == TC): constant shared-memory offsets (see the forward)
+template <class M, int G, bool DIAG, class R, int TC = 0>
 __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 || DIAG ? 4 : 3)) : 2) ilqr_backward_kernel(const BwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
@@ -78,9 +79,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   const int pid = blockIdx.x * args.gpb + grp;
   if (grp >= args.gpb || pid >= args.B) return;
   const unsigned gm = group_mask<G>();
-  const int T = args.T;
+  const int T = TC > 0 ? TC : args.T;
   const Lay L = Lay::make(T);
-  unsigned char* base = smem_raw + (size_t)grp * args.smem_stride;
+  const int sstride = TC > 0 ? group_stride<Lay>(TC, G) : args.smem_stride;
+  unsigned char* base = smem_raw + (size_t)grp * sstride;
   R* Xs = (R*)(base + L.oX);    // rows of LDA
   R* Us = (R*)(base + L.oU);    // rows of LDB
   R* Ka = (R*)(base + L.oK);    // [t][r][LDA]
@@ -268,9 +270,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         }
       }
       __syncwarp(gm);
-      ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc, quu, true);
-      __syncwarp(gm);
-      ric_symmetrize<M, DIAG, R, G, RPL>(S, lane, vxx);
+      if constexpr (DIAG) {  // symmetric C: no symmetrisation pass needed (ric_Vxx_lean_regs)
+        ric_Vxx_lean_regs<M, DIAG, R, G, RPL>(S, lane, qxx, quxc, vxx);
+      } else {
+        ric_Vxx_rows<M, DIAG, R, G, RPL>(S, lane, qxx, kcol, quxc, quu, true);
+        __syncwarp(gm);
+        ric_symmetrize<M, DIAG, R, G, RPL>(S, lane, vxx);
+      }
     }
     cp_async_wait_all();
     __syncwarp(gm);
@@ -364,7 +370,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
                 const R v = ca ? R(0) : R(0.5) * (da * za + za * da);
                 dCo[t * NZ + a] = v + R(0.5) * sJ * za * za;
               } else {
-                R* row = dCo + ((size_t)t * NZ + a) * NZ;
+                // row a of dC_t goes to the (free) cost staging buffer first; the group then
+                // writes the whole NZ x NZ block with consecutive lanes on consecutive words
+                R* row = S.Rb + a * NZ;
                 const R hs = R(0.5) * sJ * za;
 #pragma unroll
                 for (int b = 0; b < NZ; b++) {
@@ -374,6 +382,15 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
                 }
               }
             }
+          }
+        }
+        if constexpr (!DIAG) {
+          if (dCo) {
+            __syncwarp(gm);
+            R* blk = dCo + (size_t)t * NZ * NZ;
+#pragma unroll
+            for (int e0 = 0; e0 < NZ * NZ; e0 += G)
+              if (e0 + lane < NZ * NZ) blk[e0 + lane] = S.Rb[e0 + lane];
           }
         }
       }

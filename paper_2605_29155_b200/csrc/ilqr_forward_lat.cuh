@@ -27,7 +27,7 @@ struct LatLayout {
   using D = Dims<M, DIAG, R>;
   int nbuf;
   int oPe, oX, oU, okg, oJc, oPr, oAs, oBs, oMA, oNB, oQxx, oQuxT, oQuu, oqu, oqx, oVx, oVxx, oN, oKT, oK, ozs,
-      oL, oC, oc, total;
+      oL, oC, oc, oAT, oBT, ogz, obd, total;
   __host__ __device__ static LatLayout make(int T, int n_alpha) {
     LatLayout L;
     L.nbuf = 1 + n_alpha;
@@ -58,6 +58,11 @@ struct LatLayout {
     L.oL = take((D::NU * D::NU + 4 * D::NU + 8) * s);  // factor, inverses, du, flags
     L.oC = take(T * D::NCSP * s);
     L.oc = take(T * D::ZLD * s);
+    // every stage's A_t, B_t and g_t = C_t z_t + c_t, evaluated in parallel before the sweep
+    L.oAT = take(T * D::NX * D::LDA * s);
+    L.oBT = take(T * D::NX * D::LDB * s);
+    L.ogz = take(T * D::ZLD * s);
+    L.obd = take(T * 2 * D::NU * 8);  // per stage: u_min - U_t, u_max - U_t (double)
     L.total = o;
     return L;
   }
@@ -78,6 +83,7 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ LatState st;
   __shared__ double Jc[8];
+  __shared__ double Jw[8];  // per-warp partial candidate costs
   __shared__ int deadc[8];
 
   const int pid = blockIdx.x;
@@ -109,6 +115,10 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
   R* Lf = (R*)(base + L.oL);  // [NU*NU] factor | [NU] inv | [NU] du | [NU] free | [NU] lo-hi scratch
   R* Cs = (R*)(base + L.oC);
   R* cs = (R*)(base + L.oc);
+  R* AT = (R*)(base + L.oAT);  // [t][NX][LDA]
+  R* BT = (R*)(base + L.oBT);  // [t][NX][LDB]
+  R* gz = (R*)(base + L.ogz);  // [t][ZLD]
+  double* bd = (double*)(base + L.obd);  // [t][lo(NU) | hi(NU)] bound offsets of the QP
   const int XB = (T + 1) * XLD, UB = T * ULD;  // buffer strides
   auto Xbuf = [&](int b) { return Xb + b * XB; };
   auto Ubuf = [&](int b) { return Ub + b * UB; };
@@ -169,6 +179,9 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
       kg[(e / NU) * ULD + r] = 0.0;
     }
   }
+  __syncthreads();  // As / Bs (constant structure) complete
+  for (int e = tid; e < T * NX * LDA; e += kLatThreads) AT[e] = As[e % (NX * LDA)];
+  for (int e = tid; e < T * NX * LDB; e += kLatThreads) BT[e] = Bs[e % (NX * LDB)];
   R* Ko = args.K ? (R*)args.K + (size_t)pid * T * NU * NX : nullptr;
   R* ahist = args.alpha_hist ? (R*)args.alpha_hist + (size_t)pid * args.K_max : nullptr;
   R* jhist = args.J_hist ? (R*)args.J_hist + (size_t)pid * (args.K_max + 1) : nullptr;
@@ -217,31 +230,6 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
     return part;
   };
 
-  // lane i < NZ's share z_i (0.5 (C_t z)_i + c_i) of the stage cost, branch-free (lanes >= NZ
-  // read row NZ-1 and contribute 0) so the scheduler can overlap it with the dynamics; the
-  // line search sums these shares per lane over the horizon and reduces once at the end.
-  auto lane_cost = [&](const R* C_t, const R* c_t, const double (&x)[NX], const double (&u)[NU]) -> double {
-    double z[NZ];
-#pragma unroll
-    for (int i = 0; i < NX; i++) z[i] = x[i];
-#pragma unroll
-    for (int i = 0; i < NU; i++) z[NX + i] = u[i];
-    const int row = lane < NZ ? lane : NZ - 1;
-    double zi = 0.0;
-#pragma unroll
-    for (int k = 0; k < NZ; k++)
-      if (lane == k) zi = z[k];
-    if constexpr (DIAG) {
-      return 0.5 * zi * ((double)C_t[row] * zi) + (double)c_t[row] * zi;
-    } else {
-      R crow[NZ];
-      lds_row<NZ>(C_t + row * ZLD, crow);
-      double ra[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int j = 0; j < NZ; j++) ra[j & 3] += (double)crow[j] * z[j];
-      return 0.5 * zi * ((ra[0] + ra[1]) + (ra[2] + ra[3])) + (double)c_t[row] * zi;
-    }
-  };
 
   // =========================== initial rollout (kernels.py:161-178), warp 0 =========
   if (warp == 0) {
@@ -307,33 +295,53 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
     for (int e = tid; e < NX * LDA; e += kLatThreads) Vxx[e] = R(0);
     for (int e = tid; e < LDA; e += kLatThreads) Vx[e] = R(0);
     __syncthreads();
+    // Stage-parallel prologue: every stage's Jacobians (thread t < T: the state-dependent
+    // entries of A_t, B_t at the nominal) and cost gradient g_t = C_t z_t + c_t (one thread
+    // per entry), so the sequential stages below carry only the Riccati recursion.
+    if constexpr (!M::kLinearParams) {
+      for (int t = tid; t < T; t += kLatThreads) {
+        R xr[NX], ur[NU];
+#pragma unroll
+        for (int i = 0; i < NX; i++) xr[i] = (R)Xn[t * XLD + i];
+#pragma unroll
+        for (int i = 0; i < NU; i++) ur[i] = (R)Un[t * ULD + i];
+        M::template jac_vary<R>(P_r, dt_r, xr, ur, AT + t * NX * LDA, LDA, BT + t * NX * LDB, LDB);
+      }
+    }
+    for (int e = tid; e < T * NZ; e += kLatThreads) {
+      const int t = e / NZ, a = e - (e / NZ) * NZ;
+      const R* C_t = Cs + t * NCSP;
+      R s0 = cs[t * ZLD + a], s1 = R(0);
+      if constexpr (DIAG) {
+        s0 += C_t[a] * (R)(a < NX ? Xn[t * XLD + a] : Un[t * ULD + a - NX]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NZ; j++) {
+          const R p = C_t[a * ZLD + j] * (R)(j < NX ? Xn[t * XLD + j] : Un[t * ULD + j - NX]);
+          if (j & 1) s1 += p; else s0 += p;
+        }
+      }
+      gz[t * ZLD + a] = s0 + s1;
+    }
+    for (int e = tid; e < T * NU; e += kLatThreads) {
+      const int t = e / NU, i = e - (e / NU) * NU;
+      bd[t * 2 * NU + i] = args.u_min[i] - Un[t * ULD + i];
+      bd[t * 2 * NU + NU + i] = args.u_max[i] - Un[t * ULD + i];
+    }
+    __syncthreads();
+    LAT_MARK(1);
     bool failed_sweep = false;
     for (int t = T - 1; t >= 0; t--) {
       const R* C_t = Cs + t * NCSP;
-      const R* c_t = cs + t * ZLD;
-      // P1: state-dependent Jacobian entries (warp 0), z_t in R
-      if (warp == 0) {
-        if constexpr (!M::kLinearParams) {
-          R xr[NX], ur[NU];
-#pragma unroll
-          for (int i = 0; i < NX; i++) xr[i] = (R)Xn[t * XLD + i];
-#pragma unroll
-          for (int i = 0; i < NU; i++) ur[i] = (R)Un[t * ULD + i];
-          M::template jac_vary<R>(P_r, dt_r, xr, ur, As, LDA, Bs, LDB);
-        }
-      } else if (tid - 32 < NZ) {
-        const int i = tid - 32;
-        zs[i] = (R)(i < NX ? Xn[t * XLD + i] : Un[t * ULD + i - NX]);
-      }
-      __syncthreads();
-      LAT_MARK(1);
-      // P2: MA = Vxx A, NB = Vxx B, qx = gz_x + A'Vx, qu = gz_u + B'Vx  (kernels.py:395-421)
+      const R* At = AT + t * NX * LDA;
+      const R* Bt = BT + t * NX * LDB;
+      // P2: MA = Vxx A, NB = Vxx B, qx = g_x + A'Vx, qu = g_u + B'Vx  (kernels.py:395-421)
       if (tid < NX * NX) {
         const int a = tid / NX, b = tid % NX;
         R s0 = R(0), s1 = R(0);
 #pragma unroll
         for (int r = 0; r < NX; r++) {
-          const R p = Vxx[a * LDA + r] * As[r * LDA + b];
+          const R p = Vxx[a * LDA + r] * At[r * LDA + b];
           if (r & 1) s1 += p; else s0 += p;
         }
         MA[a * LDA + b] = s0 + s1;
@@ -341,27 +349,19 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
         const int e = tid - NX * NX, a = e / NU, i = e % NU;
         R s = R(0);
 #pragma unroll
-        for (int r = 0; r < NX; r++) s += Vxx[a * LDA + r] * Bs[r * LDB + i];
+        for (int r = 0; r < NX; r++) s += Vxx[a * LDA + r] * Bt[r * LDB + i];
         NB[a * LDB + i] = s;
       } else if (tid < NX * NX + NX * NU + NZ) {
         const int a = tid - NX * NX - NX * NU;
-        R s0 = c_t[a], s1 = R(0);
-        if constexpr (DIAG) {
-          s0 += C_t[a] * zs[a];
-        } else {
-#pragma unroll
-          for (int j = 0; j < NZ; j++) {
-            const R p = C_t[a * ZLD + j] * zs[j];
-            if (j & 1) s1 += p; else s0 += p;
-          }
-        }
+        const R s0 = gz[t * ZLD + a];
+        R s1 = R(0);
         if (a < NX) {
 #pragma unroll
-          for (int r = 0; r < NX; r++) s1 += As[r * LDA + a] * Vx[r];
+          for (int r = 0; r < NX; r++) s1 += At[r * LDA + a] * Vx[r];
           qx[a] = s0 + s1;
         } else {
 #pragma unroll
-          for (int r = 0; r < NX; r++) s1 += Bs[r * LDB + (a - NX)] * Vx[r];
+          for (int r = 0; r < NX; r++) s1 += Bt[r * LDB + (a - NX)] * Vx[r];
           qu[a - NX] = s0 + s1;
         }
       }
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
         else s0 = C_t[a * ZLD + b];
 #pragma unroll
         for (int r = 0; r < NX; r++) {
-          const R p = As[r * LDA + a] * MA[r * LDA + b];
+          const R p = At[r * LDA + a] * MA[r * LDA + b];
           if (r & 1) s1 += p; else s0 += p;
         }
         Qxx[a * LDA + b] = s0 + s1;
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
         if constexpr (DIAG) s = R(0);
         else s = C_t[(NX + i) * ZLD + b];
 #pragma unroll
-        for (int r = 0; r < NX; r++) s += Bs[r * LDB + i] * MA[r * LDA + b];
+        for (int r = 0; r < NX; r++) s += Bt[r * LDB + i] * MA[r * LDA + b];
         QuxT[b * LDB + i] = s;
       } else if (tid < NX * NX + NX * NU + NU * NU) {
         const int e = tid - NX * NX - NX * NU, i = e / NU, j = e % NU;
@@ -393,45 +393,74 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
         if constexpr (DIAG) s = (i == j) ? C_t[NX + i] : R(0);
         else s = C_t[(NX + i) * ZLD + NX + j];
 #pragma unroll
-        for (int r = 0; r < NX; r++) s += Bs[r * LDB + i] * NB[r * LDB + j];
+        for (int r = 0; r < NX; r++) s += Bt[r * LDB + i] * NB[r * LDB + j];
         Quu[i * LDB + j] = s;
       }
       __syncthreads();
       LAT_MARK(3);
-      // P4: lambda-regularised box QP on the control block, one thread (kernels.py:440-489)
-      if (tid == 0) {
+      // P4: the lambda-regularised box QP on the control block (kernels.py:440-489), run
+      // redundantly by the NX lanes that then form one K column each and the V_x update
+      // (kernels.py:481-498): one phase, the factor stays in registers.
+      if (tid < NX) {
+        const int b = tid;
         R quu[NU][NU], qv[NU], lo[NU], hi[NU], du[NU];
-        bool fr[NU], lam0;
+        bool fr[NU], lam0 = true;
         Chol<NU, R> ch;
-        double ud[NU];
+        double lod[NU], hid[NU];
 #pragma unroll
         for (int i = 0; i < NU; i++) {
 #pragma unroll
           for (int j = 0; j < NU; j++) quu[i][j] = Quu[i * LDB + j];
           qv[i] = qu[i];
-          ud[i] = Un[t * ULD + i];
-          lo[i] = (R)(args.u_min[i] - ud[i]);
-          hi[i] = (R)(args.u_max[i] - ud[i]);
+          lod[i] = bd[t * 2 * NU + i];
+          hid[i] = bd[t * 2 * NU + NU + i];
+          lo[i] = (R)lod[i];
+          hi[i] = (R)hid[i];
         }
-        const bool ok = stage_qp<NU, R>(quu, qv, lo, hi, args.boxqp_max_iter, (R)args.boxqp_tol, du, fr, ch, lam0);
-        st.ok = ok;
-        st.lam0 = lam0;
+        // straight-line interior fast path; the full lambda / projected-Newton solve only
+        // when it does not apply (the box binds, or Quu is not positive definite)
+        bool ok = qp_interior<NU, R>(quu, qv, lo, hi, (R)args.boxqp_tol, du, fr, ch);
+        if (!ok) ok = stage_qp<NU, R>(quu, qv, lo, hi, args.boxqp_max_iter, (R)args.boxqp_tol, du, fr, ch, lam0);
+        if (b == 0) {
+          st.ok = ok;
+          st.lam0 = lam0;
+          if (ok) {
+#pragma unroll
+            for (int i = 0; i < NU; i++) {
+              double kd = (double)du[i];  // bound snapping (see ilqr_forward_kernel)
+              if (du[i] <= lo[i]) kd = lod[i];
+              else if (du[i] >= hi[i]) kd = hid[i];
+              kg[t * ULD + i] = kd;
+            }
+          } else {
+            st.fail_t = t;
+            st.active = 0;
+          }
+        }
         if (ok) {
+          R quxc[NU], rhs[NU], sol[NU], kcol[NU];
 #pragma unroll
           for (int i = 0; i < NU; i++) {
-            double kd = (double)du[i];  // bound snapping (see ilqr_forward_kernel)
-            if (du[i] <= lo[i]) kd = args.u_min[i] - ud[i];
-            else if (du[i] >= hi[i]) kd = args.u_max[i] - ud[i];
-            kg[t * ULD + i] = kd;
-#pragma unroll
-            for (int j = 0; j < NU; j++) Lf[i * NU + j] = ch.L[i][j];
-            Lf[NU * NU + i] = ch.inv[i];
-            Lf[NU * NU + NU + i] = du[i];
-            Lf[NU * NU + 2 * NU + i] = fr[i] ? R(1) : R(0);
+            quxc[i] = QuxT[b * LDB + i];
+            rhs[i] = fr[i] ? quxc[i] : R(0);
           }
-        } else {
-          st.fail_t = t;
-          st.active = 0;
+          chol_solve<NU, R>(ch, rhs, sol);
+#pragma unroll
+          for (int i = 0; i < NU; i++) {
+            kcol[i] = fr[i] ? -sol[i] : R(0);
+            KT[b * LDB + i] = kcol[i];
+            Ks[(t * NU + i) * LDA + b] = kcol[i];
+            if (Ko) Ko[(t * NU + i) * NX + b] = kcol[i];
+          }
+          R sv = qx[b];
+#pragma unroll
+          for (int r = 0; r < NU; r++) {
+            R rowq = R(0);
+#pragma unroll
+            for (int q = 0; q < NU; q++) rowq += quu[r][q] * du[q];
+            sv += kcol[r] * (rowq + qv[r]) + quxc[r] * du[r];
+          }
+          Vx[b] = sv;
         }
       }
       __syncthreads();
@@ -441,77 +470,40 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
         break;
       }
       const bool lam0 = st.lam0 != 0;
-      // P5: K columns (free rows), Vx update (kernels.py:481-498)
-      if (tid < NX) {
-        const int b = tid;
-        Chol<NU, R> ch;
-        R du[NU], quxc[NU], rhs[NU], sol[NU], kcol[NU], quu[NU][NU];
-        bool fr[NU];
-#pragma unroll
-        for (int i = 0; i < NU; i++) {
-#pragma unroll
-          for (int j = 0; j < NU; j++) {
-            ch.L[i][j] = Lf[i * NU + j];
-            quu[i][j] = Quu[i * LDB + j];
-          }
-          ch.inv[i] = Lf[NU * NU + i];
-          du[i] = Lf[NU * NU + NU + i];
-          fr[i] = Lf[NU * NU + 2 * NU + i] != R(0);
-          quxc[i] = QuxT[b * LDB + i];
-          rhs[i] = fr[i] ? quxc[i] : R(0);
-        }
-        chol_solve<NU, R>(ch, rhs, sol);
-#pragma unroll
-        for (int i = 0; i < NU; i++) {
-          kcol[i] = fr[i] ? -sol[i] : R(0);
-          KT[b * LDB + i] = kcol[i];
-          Ks[(t * NU + i) * LDA + b] = kcol[i];
-          if (Ko) Ko[(t * NU + i) * NX + b] = kcol[i];
-        }
-        R s = qx[b];
-#pragma unroll
-        for (int r = 0; r < NU; r++) {
-          R rowq = R(0);
-#pragma unroll
-          for (int q = 0; q < NU; q++) rowq += quu[r][q] * du[q];
-          s += kcol[r] * (rowq + qu[r]) + quxc[r] * du[r];
-        }
-        Vx[b] = s;
-      }
-      __syncthreads();
-      LAT_MARK(5);
-      // P6: N = Qxx + Qux'K (lean) or the full value update (kernels.py:499-507)
+      // P5: V_xx = (N + N')/2 with N = Qxx + Qux'K (lean) or the full value update
+      // (kernels.py:499-512); thread (a, b) forms both N[a,b] and N[b,a] (no extra phase)
       if (tid < NX * NX) {
         const int a = tid / NX, b = tid % NX;
-        R s = Qxx[a * LDA + b];
-        if (lam0) {
+        auto nval = [&](int i, int j) -> R {
+          R s = Qxx[i * LDA + j];
+          if (lam0) {
 #pragma unroll
-          for (int r = 0; r < NU; r++) s += QuxT[a * LDB + r] * KT[b * LDB + r];
-        } else {
+            for (int r = 0; r < NU; r++) s += QuxT[i * LDB + r] * KT[j * LDB + r];
+          } else {
 #pragma unroll
-          for (int r = 0; r < NU; r++) {
-            R kq = R(0);
+            for (int r = 0; r < NU; r++) {
+              R kq = R(0);
 #pragma unroll
-            for (int q = 0; q < NU; q++) kq += Quu[r * LDB + q] * KT[b * LDB + q];
-            s += (KT[a * LDB + r] * kq + KT[a * LDB + r] * QuxT[b * LDB + r]) + QuxT[a * LDB + r] * KT[b * LDB + r];
+              for (int q = 0; q < NU; q++) kq += Quu[r * LDB + q] * KT[j * LDB + q];
+              s += (KT[i * LDB + r] * kq + KT[i * LDB + r] * QuxT[j * LDB + r]) + QuxT[i * LDB + r] * KT[j * LDB + r];
+            }
           }
-        }
-        Nn[a * LDA + b] = s;
-      }
-      __syncthreads();
-      LAT_MARK(6);
-      // P7: V_xx = (N + N') / 2 (kernels.py:510-512)
-      if (tid < NX * NX) {
-        const int a = tid / NX, b = tid % NX;
-        Vxx[a * LDA + b] = R(0.5) * (Nn[a * LDA + b] + Nn[b * LDA + a]);
+          return s;
+        };
+        Vxx[a * LDA + b] = R(0.5) * (nval(a, b) + nval(b, a));
       }
       if (tid == 0) st.k_lo = t;
       __syncthreads();
+      LAT_MARK(5);
     }
     (void)failed_sweep;
     LAT_MARK(7);
 
     // --------------------- line search: one warp per step size -------------------
+    // Phase A: warp a rolls candidate a out (feedback law + dynamics only, the chain that
+    // is inherently sequential in t) into its own trajectory buffer. Phase B: all 8 warps
+    // evaluate every candidate's stage costs in parallel and reduce them (the costs are off
+    // the state recursion, so they no longer sit on its critical path).
     const int act = st.active;
     if (act && warp < NA) {
       const int a = warp;
@@ -521,7 +513,6 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
       double* Uc = Ubuf(cb);
       double x[NX];
       lds_row_d<NX>(Xn, x);
-      double Jl = 0.0;  // this lane's share of the candidate cost, summed over t
       bool dm = false;
       for (int t = 0; t < T; t++) {
         // nominal row, controls, gains: independent of the candidate state
@@ -539,36 +530,76 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
 #pragma unroll
         for (int q = 0; q < NU; q++) u[q] = __shfl_sync(0xffffffffu, v, q);
         double xn[NX];
-        step_e<M, R>(P_e, dt_e, As, LDA, Bs, LDB, x, u, xn);  // critical path first
-        Jl += lane_cost(Cs + t * NCSP, cs + t * ZLD, x, u);   // overlaps the dynamics
+        step_e<M, R>(P_e, dt_e, As, LDA, Bs, LDB, x, u, xn);
         if (lane < NU) Uc[t * ULD + lane] = v;
+        double xl = x[0];  // lane i stores x_i: a select chain and one store
 #pragma unroll
-        for (int i = 0; i < NX; i++)
-          if (lane == i) Xc[t * XLD + i] = x[i];
-        bool fin = true;
+        for (int i = 1; i < NX; i++) xl = lane == i ? x[i] : xl;
+        if (lane < NX) Xc[t * XLD + lane] = xl;
 #pragma unroll
-        for (int i = 0; i < NX; i++) {
-          fin &= finite_(xn[i]);
-          x[i] = xn[i];
-        }
-        dm |= !fin;
+        for (int i = 0; i < NX; i++) x[i] = xn[i];
       }
+      // Dead candidates (kernels.py:569-574): a non-finite x_{t+1} for t < T-1 makes the
+      // stage-(t+1) cost non-finite (z_i * (C z)_i with z_i = inf / nan), which phase B
+      // detects; x_T has no stage cost and is checked here. So the per-stage finiteness
+      // tests of the reference are decided exactly, off the rollout's critical path.
+      double xl = x[0];
 #pragma unroll
-      for (int i = 0; i < NX; i++)
-        if (lane == i) Xc[T * XLD + i] = x[i];
-      // one reduction per candidate; a non-finite stage cost leaves a non-finite sum (dead)
-      if (lane >= NZ) Jl = 0.0;
+      for (int i = 1; i < NX; i++) xl = lane == i ? x[i] : xl;
+      if (lane < NX) Xc[T * XLD + lane] = xl;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) Jl += __shfl_xor_sync(0xffffffffu, Jl, off);
-      const double Jm = Jl;
-      dm |= !finite_(Jm);
-      if (lane == 0) {
-        Jc[a] = dm ? INFINITY : Jm;
-        deadc[a] = dm;
-      }
+      for (int i = 0; i < NX; i++) dm |= !finite_(x[i]);
+      if (lane == 0) deadc[a] = dm;
     }
     __syncthreads();
     LAT_MARK(8);
+    if (act) {
+      // Phase B: (candidate, stage, row) items; WPC warps per candidate share its T * NZ rows
+      const int wpc = 8 / NA;  // NA <= 8
+      const int a = warp / wpc;
+      double part = 0.0;
+      if (a < NA) {
+        const int cb = (nom + 1 + a) % L.nbuf;
+        const double* Xc = Xbuf(cb);
+        const double* Uc = Ubuf(cb);
+        const int P = wpc * 32, s0 = (warp - a * wpc) * 32 + lane;
+        for (int e = s0; e < T * NZ; e += P) {
+          const int t = e / NZ, i = e - (e / NZ) * NZ;
+          double x[NX], u[NU];
+          lds_row_d<NX>(Xc + t * XLD, x);
+          lds_row_d<NU>(Uc + t * ULD, u);
+          const R* C_t = Cs + t * NCSP;
+          const R* c_t = cs + t * ZLD;
+          const double zi = i < NX ? Xc[t * XLD + i] : Uc[t * ULD + i - NX];
+          if constexpr (DIAG) {
+            part += 0.5 * zi * ((double)C_t[i] * zi) + (double)c_t[i] * zi;
+          } else {
+            R crow[NZ];
+            lds_row<NZ>(C_t + i * ZLD, crow);
+            double ra[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < NX; j++) ra[j & 3] += (double)crow[j] * x[j];
+#pragma unroll
+            for (int j = 0; j < NU; j++) ra[(NX + j) & 3] += (double)crow[NX + j] * u[j];
+            part += 0.5 * zi * ((ra[0] + ra[1]) + (ra[2] + ra[3])) + (double)c_t[i] * zi;
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+        if (lane == 0) Jw[warp] = part;
+      }
+      __syncthreads();
+      if (tid < NA) {  // fixed-order sum of the candidate's warp partials (repeatable); a
+                       // non-finite state or stage cost makes the candidate dead
+        double J = 0.0;
+        for (int w = 0; w < wpc; w++) J += Jw[tid * wpc + w];
+        const bool dm = deadc[tid] != 0 || !finite_(J);
+        deadc[tid] = dm;
+        Jc[tid] = dm ? INFINITY : J;
+      }
+    }
+    __syncthreads();
+    LAT_MARK(6);
     // ------------------------- epilogue (ilqr.py:216-244) -----------------------
     if (tid == 0) {
       if (act) st.iterations = it + 1;
@@ -607,8 +638,8 @@ __global__ void __launch_bounds__(kLatThreads, 2) ilqr_forward_lat_kernel(const 
 
 #ifdef DMPC_LAT_PROF
   if (tid == 0 && pid == 0)
-    printf("lat prof cycles: P1 %lld P2 %lld P3 %lld P4(QP) %lld P5 %lld P6 %lld P7 %lld sweep-end %lld LS %lld\n",
-           prof[1], prof[2], prof[3], prof[4], prof[5], prof[6], prof[0], prof[7], prof[8]);
+    printf("lat prof cycles: prologue %lld P2 %lld P3 %lld P4(QP+K) %lld P5(V) %lld sweep-end %lld "
+           "LS-rollout %lld LS-costs %lld\n", prof[1], prof[2], prof[3], prof[4], prof[5], prof[7], prof[8], prof[6]);
 #endif
   // ================================ outputs ====================================
   if (jhist && tid == 0)

@@ -207,6 +207,9 @@ int bwd_impl(const DiffMPCProblem* p, const DiffMPCBackwardIO* io, cudaStream_t 
   a.dC = io->dC; a.dc = io->dc; a.dx0 = io->dx0; a.dtheta = io->dtheta; a.dX = io->dX; a.dU = io->dU;
   a.fail_t = io->fail_t;
   auto kern = ilqr_backward_kernel<M, G, DIAG, R>;
+  if constexpr (sizeof(R) == 4) {
+    if (p->T == 10) kern = ilqr_backward_kernel<M, G, DIAG, R, 10>;
+  }
   if (plan<BwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
   const int smem = a.gpb * a.smem_stride;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
