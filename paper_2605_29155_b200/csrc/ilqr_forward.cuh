@@ -602,15 +602,16 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           lsp.release(t);
           double xn[NX];
           step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xc, u, xn);
-          bool fin = true;
 #pragma unroll
-          for (int i = 0; i < NX; i++) {
-            fin &= finite_(xn[i]);
-            xc[i] = xn[i];
-          }
-          dm |= !fin;  // dead candidates keep stepping (harmlessly) to stay in lockstep
-          __syncwarp(gm);
+          for (int i = 0; i < NX; i++) xc[i] = xn[i];
+          __syncwarp(gm);  // dead candidates keep stepping (harmlessly) to stay in lockstep
         }
+        // dead candidates (kernels.py:569-574): a non-finite x_{t+1}, t < T-1, makes the
+        // stage-(t+1) cost non-finite (z_i (C z)_i with z_i inf / nan; checked on the sum
+        // below), and x_T, which no stage cost sees, is checked here: the reference's
+        // per-stage tests, decided once per candidate
+#pragma unroll
+        for (int i = 0; i < NX; i++) dm |= !finite_(xc[i]);
         if (shadow) {
 #pragma unroll
           for (int i = 0; i < NX; i++)
