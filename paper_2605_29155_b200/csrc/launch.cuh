@@ -141,6 +141,11 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   auto kern = lock ? ilqr_forward_kernel<M, G, DIAG, R, true> : ilqr_forward_kernel<M, G, DIAG, R, false>;
   if constexpr (sizeof(R) == 4) {  // the bench horizon with compile-time shared-memory offsets
     if (p->T == 10) kern = lock ? ilqr_forward_kernel<M, G, DIAG, R, true, 10> : ilqr_forward_kernel<M, G, DIAG, R, false, 10>;
+    if constexpr (std::is_same_v<M, Quad13>) {  // the config-5 sweep horizons of the BASELINE model
+      if (p->T == 5 && !lock) kern = ilqr_forward_kernel<M, G, DIAG, R, false, 5>;
+      if (p->T == 20 && lock) kern = ilqr_forward_kernel<M, G, DIAG, R, true, 20>;
+      if (p->T == 40 && lock) kern = ilqr_forward_kernel<M, G, DIAG, R, true, 40>;
+    }
   }
   int per_sm = 1;
   if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)) return -1;

@@ -16,7 +16,7 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+sys.path[:0] = [os.environ.get("DIFFMPC_PKG_ROOT", ROOT), os.path.join(ROOT, "oracle")]  # env: A/B another copy
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
