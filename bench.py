@@ -382,6 +382,11 @@ def run_ours(args):
                   "how": "same inputs and settings, float64 kernels; rank 0, median of 5 after 3 warm-up"}
         del d64, o64
 
+    # ---- the AC-MPC layer's diagonal cost layout, device and end to end (rank 0) ----
+    diag_leg = None
+    if args.layout == "dense" and rank == 0:
+        diag_leg = diag_layout_leg(pb, dtype, dev, max(10, args.steps // 2), max(3, args.warmup // 2))
+
     # ---- self-check of the timed outputs against the oracle (untimed, bounded sample) ----
     parity = None
     if rank == 0:
@@ -428,7 +433,8 @@ def run_ours(args):
                              "hbm_gbs": bytes_fwd / (fwd_ms * 1e-3) / 1e9},
                 "clocks": clk.summary(),
                 "parity": parity,
-                "reference_precision": f64leg}
+                "reference_precision": f64leg,
+                "diag_layout": diag_leg}
         if not args.no_cpu_baseline and world == 1:
             r, thr, sample = cpu_oracle_rate(pb, seconds=12.0)
             line["cpu_baseline"] = {"value": r, "unit": "solves/s", "cores": thr, "kind": "port",
@@ -437,6 +443,82 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def diag_layout_leg(pb, dtype, dev, steps, warmup, NS=3):
+    """The same problems in the AC-MPC layer's diagonal cost layout (C_t = diag(d_t),
+    MpcSolver.solve_diag, policy.py:214-222): device-resident step (L2 flushed between steps:
+    the inputs fit in L2) and end to end from pinned host buffers (3-stream pipeline)."""
+    import torch
+
+    from paper_2605_29155_b200 import solver
+
+    model, st = pb.model, pb.settings
+    B, T, n, m = pb.B, st.T, model.n_x, model.n_u
+    dU = np.zeros((B, T, m))
+    dU[:, 0, :] = 1.0
+    host = {"x0": pb.x0, "C": pb.diag, "c": pb.c, "U_warm": pb.U_warm, "dLdU": dU}
+    pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dtype).pin_memory() for k, v in host.items()}
+    dev_in = {k: v.to(dev) for k, v in pinned.items()}
+    flush = torch.empty(int(256e6), dtype=torch.uint8, device=dev)
+
+    def step(inp):
+        out = solver.solve_raw(model, st, inp["x0"], inp["C"], inp["c"], inp["U_warm"], dtype=dtype)
+        g = solver.backward_raw(model, st, inp["C"], inp["c"], out.X, out.U, None, inp["dLdU"], dtype=dtype)
+        return out, g
+
+    for _ in range(warmup):
+        step(dev_in)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        step(dev_in)
+        b.record()
+        ts.append((a, b))
+    torch.cuda.synchronize()
+    dev_ms = float(np.mean([a.elapsed_time(b) for a, b in ts]))
+    streams = [torch.cuda.Stream(device=dev) for _ in range(NS)]
+    res = [{"U": torch.empty((B, T, m), dtype=dtype).pin_memory(), "J": torch.empty((B,), dtype=dtype).pin_memory(),
+            "dC": torch.empty((B, T, n + m), dtype=dtype).pin_memory(),
+            "dc": torch.empty((B, T, n + m), dtype=dtype).pin_memory(),
+            "dx0": torch.empty((B, n), dtype=dtype).pin_memory()} for _ in range(NS)]
+    h2d = sum(v.numel() * v.element_size() for v in pinned.values())
+    d2h = sum(v.numel() * v.element_size() for v in res[0].values())
+
+    def e2e_step(k):
+        s_ = streams[k % NS]
+        with torch.cuda.stream(s_):
+            out, g = step({kk: v.to(dev, non_blocking=True) for kk, v in pinned.items()})
+            r = res[k % NS]
+            for name, t in (("U", out.U), ("J", out.J), ("dC", g.dC), ("dc", g.dc), ("dx0", g.dx0)):
+                r[name].copy_(t, non_blocking=True)
+
+    for k in range(2 * NS):
+        e2e_step(k)
+    torch.cuda.synchronize()
+    main = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(main)
+    for s_ in streams:
+        s_.wait_event(a)
+    K = max(3 * NS, steps)
+    for k in range(K):
+        e2e_step(k)
+    for s_ in streams:
+        e = torch.cuda.Event()
+        e.record(s_)
+        main.wait_event(e)
+    b.record(main)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / K
+    return {"value": B / (dev_ms * 1e-3), "unit": "solves/s", "ms_per_step": dev_ms,
+            "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "solves/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "how": f"same problems with C_t = diag(d_t) (B,T,nz) in and diag(dC_t) out; rank 0; L2 flushed "
+                   f"between device steps; {NS}-stream pipeline end to end"}
 
 
 def self_check(pb, out, g, dtype, layout, n=512):

@@ -125,6 +125,20 @@ DMPC_DEV void step_e(const double* P, double dt, const R* As, int lda, const R* 
   }
 }
 
+// dst[i] = v[i] for the entries i = j (mod S) this lane owns (lane j of S): a select chain per
+// owned entry and one store, instead of N predicated stores
+template <int N, int S>
+DMPC_DEV void store_owned(double* dst, const double (&v)[N], int j) {
+#pragma unroll
+  for (int i0 = 0; i0 < N; i0 += S) {
+    double val = v[i0];
+#pragma unroll
+    for (int l = 1; l < S; l++)
+      if (i0 + l < N) val = (j == l) ? v[i0 + l] : val;
+    if (i0 + j < N) dst[i0 + j] = val;
+  }
+}
+
 // Feedback law v + K_r (x - xbar) in double (kernels.py:560-568) as two independent DFMA
 // chains; the line search and the winner's re-roll share it, so the re-roll reproduces
 // the candidate bit for bit.
@@ -362,9 +376,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         fin &= finite_(xn[i]);
         xc[i] = xn[i];
       }
-#pragma unroll
-      for (int i = 0; i < NX; i++)
-        if ((i % G) == lane) Xn[(t + 1) * XLD + i] = xn[i];
+      store_owned<NX, G>(Xn + (t + 1) * XLD, xn, lane);
       __syncwarp(gm);
       if (!fin) {
         fail_t = t;
@@ -489,14 +501,20 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       // A coordinate the QP left on a bound is stored as the double-precision bound
       // offset (u_min - U_t or u_max - U_t), exactly the value the reference's boxQP
       // clamps to, so U_t + k_t lands on the bound bit-exactly (clamp masks match).
-      if (lane == 0) {
+      {  // lane i < NU writes component i (selects instead of a lane-0 loop with branches)
+        static_assert(NU <= G, "one lane per control component");
+        const int i = lane < NU ? lane : 0;
+        R dui = du[0], loi = lo[0], hii = hi[0];
+        double udi = ud[0];
 #pragma unroll
-        for (int i = 0; i < NU; i++) {
-          double kd = (double)du[i];
-          if (du[i] <= lo[i]) kd = args.u_min[i] - ud[i];
-          else if (du[i] >= hi[i]) kd = args.u_max[i] - ud[i];
-          kg[t * ULD + i] = kd;
+        for (int q = 1; q < NU; q++) {
+          dui = i == q ? du[q] : dui;
+          loi = i == q ? lo[q] : loi;
+          hii = i == q ? hi[q] : hii;
+          udi = i == q ? ud[q] : udi;
         }
+        const double kd = dui <= loi ? args.u_min[i] - udi : (dui >= hii ? args.u_max[i] - udi : (double)dui);
+        if (lane < NU) kg[t * ULD + lane] = kd;
       }
       R kcol[RPL][NU];
 #pragma unroll
@@ -594,11 +612,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
             u[r] = (LC == 1) ? urr[r] : __shfl_sync(smask, urr[r / LC], (lane & ~(LC - 1)) + (r % LC), G);
           Jm += stage_cost(std::integral_constant<int, LC>{}, lsp.C(t), lsp.c(t), xc, u, j, smask);
           __syncwarp(gm);  // every slot has read the nominal X_t
-          if (shadow) {
-#pragma unroll
-            for (int i = 0; i < NX; i++)
-              if ((i % LC) == j) Xn[t * XLD + i] = xc[i];
-          }
+          if (shadow) store_owned<NX, LC>(Xn + t * XLD, xc, j);
           lsp.release(t);
           double xn[NX];
           step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xc, u, xn);
@@ -612,11 +626,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         // per-stage tests, decided once per candidate
 #pragma unroll
         for (int i = 0; i < NX; i++) dm |= !finite_(xc[i]);
-        if (shadow) {
-#pragma unroll
-          for (int i = 0; i < NX; i++)
-            if ((i % LC) == j) Xn[T * XLD + i] = xc[i];
-        }
+        if (shadow) store_owned<NX, LC>(Xn + T * XLD, xc, j);
         cp_async_wait_all();
         // one reduction per candidate; a non-finite stage cost leaves a non-finite sum
         Jm = sum_lanes(std::integral_constant<int, LC>{}, Jm, smask);
