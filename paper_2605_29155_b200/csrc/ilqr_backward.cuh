@@ -356,8 +356,25 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
           dzr[NX + i] = du[i];
           clr[NX + i] = cl[t * NU + i] != 0;
         }
+        // dense dC: lane a < G forms row a and mirrors its entries of the columns >= G into
+        // rows >= G (dC is exactly symmetric: the same two rounded products, summed in either
+        // order); only the (NZ-G)^2 corner is formed separately -- no second pass of all G
+        // lanes for the NZ - G rows beyond the group width
+        constexpr int NE = (!DIAG && NZ > G) ? NZ - G : 0;
 #pragma unroll
-        for (int k2 = 0; k2 < (NZ + G - 1) / G; k2++) {
+        for (int ce = 0; ce < NE * NE; ce++) {
+          const int r = G + ce / (NE > 0 ? NE : 1), q = G + ce % (NE > 0 ? NE : 1);
+          if (dCo && lane == ce % G) {
+            const bool cq = clr[q], crr = clr[r];
+            const R v = (crr || cq) ? R(0) : R(0.5) * (mul_rn(dzr[r], zr[q]) + mul_rn(zr[r], dzr[q]));
+            S.Rb[r * NZ + q] = v + (R(0.5) * sJ * zr[r]) * zr[q];
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < NE; e++)
+          if (dco && lane == e) dco[t * NZ + G + e] = (clr[G + e] ? R(0) : dzr[G + e]) + sJ * zr[G + e];
+#pragma unroll
+        for (int k2 = 0; k2 < (NE > 0 ? 1 : (NZ + G - 1) / G); k2++) {
           const int a = lane + k2 * G;
           if (a < NZ) {
             const bool isx = a < NX;
@@ -379,6 +396,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
                   // products rounded separately (no FMA contraction) so dC is exactly symmetric
                   const R v = (ca || clr[b]) ? R(0) : R(0.5) * (mul_rn(da, zr[b]) + mul_rn(za, dzr[b]));
                   row[b] = v + hs * zr[b];
+                  if (b >= G) S.Rb[b * NZ + a] = v + (R(0.5) * sJ * zr[b]) * za;  // mirror into row b
                 }
               }
             }
