@@ -298,23 +298,42 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       for (int i = 0; i < NZ; i++) part += 0.5 * z[i] * ((double)d[i] * z[i]) + (double)cc[i] * z[i];
       return part;
     } else {
-      constexpr int NR = (NZ + LCX - 1) / LCX;
+      // rows i = j + m*LCX for the NF row sets every lane of the slot owns ...
+      constexpr int NF = NZ / LCX, RE = NZ - NF * LCX;
+      double zown[NF > 0 ? NF : 1];
 #pragma unroll
-      for (int m = 0; m < NR; m++) {
+      for (int m = 0; m < NF; m++) {
         const int i = j + m * LCX;
-        if (i < NZ) {
-          R crow[NZ];
-          lds_row<NZ>(Cs + i * ZLD, crow);
-          double ra[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent DFMA chains
+        R crow[NZ];
+        lds_row<NZ>(Cs + i * ZLD, crow);
+        double ra[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent DFMA chains
 #pragma unroll
-          for (int jj = 0; jj < NZ; jj++) ra[jj & 3] += (double)crow[jj] * z[jj];
-          const double row = (ra[0] + ra[1]) + (ra[2] + ra[3]);
-          double zi = 0.0;
+        for (int jj = 0; jj < NZ; jj++) ra[jj & 3] += (double)crow[jj] * z[jj];
+        const double row = (ra[0] + ra[1]) + (ra[2] + ra[3]);
+        double zi = z[m * LCX];
 #pragma unroll
-          for (int k = 0; k < LCX; k++)
-            if (j == k && k + m * LCX < NZ) zi = z[k + m * LCX];
-          part += 0.5 * zi * row + (double)cs[i] * zi;
+        for (int k = 1; k < LCX; k++) zi = j == k ? z[k + m * LCX] : zi;
+        zown[m] = zi;
+        part += 0.5 * zi * row + (double)cs[i] * zi;
+      }
+      // ... and the RE < LCX leftover rows r split by COLUMNS over the slot's lanes (lane j
+      // takes the columns of its own rows plus leftover column NF*LCX + j), instead of one
+      // more full row pass in which only RE lanes of the slot work
+#pragma unroll
+      for (int e = 0; e < RE; e++) {
+        constexpr int r0 = NF * LCX;
+        const int r = r0 + e;
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < NF; m++) acc += (double)Cs[r * ZLD + j + m * LCX] * zown[m];
+        if (j < RE) {
+          double zl = z[r0];
+#pragma unroll
+          for (int k = 1; k < RE; k++) zl = j == k ? z[r0 + k] : zl;
+          acc += (double)Cs[r * ZLD + r0 + j] * zl;
         }
+        part += 0.5 * z[r] * acc;
+        if (j == 0) part += (double)cs[r] * z[r];
       }
       return part;
     }
