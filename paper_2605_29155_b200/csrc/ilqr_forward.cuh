@@ -439,7 +439,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       double ud[NU];
       lds_row_d<NU>(Un + t * ULD, ud);
       // z_t in the Riccati type: entry i converted once, by lane i (mod G)
-      for (int i = lane; i < NZ; i += G) S.zs[i] = (R)(i < NX ? Xn[t * XLD + i] : Un[t * ULD + i - NX]);
+#pragma unroll
+      for (int k0 = 0; k0 < NZ; k0 += G) {
+        const int i = k0 + lane;
+        if (i < NZ) S.zs[i] = (R)*(i < NX ? Xn + t * XLD + i : Un + t * ULD + (i - NX));
+      }
       __syncwarp(gm);  // previous stage done with As/Bs/MA; z_t and the staging visible
       R zv[NZ], vx[NX];
       lds_row<NZ>(S.zs, zv);

@@ -539,7 +539,7 @@ DMPC_DEV void ric_Vxx_lean_regs(const Ric<M, DIAG, R>& S, int lane, const R (&qx
         s0 += quxc[k][r] * kk[r];
         if (r + 1 < NU) s1 += quxc[k][r + 1] * kk[r + 1];
       }
-      vxx[k][bb] = row_of<G, RPL>(lane, k) < NX ? s0 + s1 : R(0);
+      vxx[k][bb] = s0 + s1;  // padding lanes (row >= NX) hold a finite copy of row NX-1; never stored
     }
   }
 }
