@@ -80,9 +80,16 @@ __host__ __device__ constexpr int group_stride(int T, int G) {
   return (Lay::make(T).total + 127) / 128 * 128 + 4 * G;
 }
 
+// stage-record buffers of the forward's pipes: double-buffered in f32 (the dense record of
+// the sweep / line search then arrives a whole stage ahead instead of half a stage; the
+// 1.4 KB per problem does not change the register-bound occupancy), single in f64 dense
+template <class M, bool DIAG, class R>
+constexpr int fwd_nbuf() { return (DIAG || sizeof(R) == 4) ? 2 : 1; }
+
 template <class M, bool DIAG, class R>
 struct FwdLayout {
   using D = Dims<M, DIAG, R>;
+  static constexpr int NB = fwd_nbuf<M, DIAG, R>();
   int oPe, oPr, oXn, oUn, oUs, okg, oKb, total;
   RicLayout<M, DIAG, R> ric;
   __host__ __device__ static constexpr FwdLayout make(int T) {
@@ -95,10 +102,11 @@ struct FwdLayout {
     L.oUs = o; o += T * D::ULD * 8;
     L.okg = o; o += T * D::ULD * 8;
     o = align_up(o, 16);
-    L.oKb = o; o += D::NBUF * D::NU * D::LDM * (int)sizeof(R);
+    L.oKb = o; o += NB * D::NU * D::LDM * (int)sizeof(R);
     o = align_up(o, 16);
     L.ric = RicLayout<M, DIAG, R>::make(o);
-    L.total = align_up(L.ric.end, 16);
+    // the record buffers are the last array of the Riccati scratch: extra ones follow it
+    L.total = align_up(L.ric.end + (NB - D::NBUF) * D::REC * (int)sizeof(R), 16);
     return L;
   }
 };
@@ -219,9 +227,10 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   // them out as packed, 16-byte aligned records (Pw); every later sweep and line search
   // stages those with 16-byte copies
   R* Pw = (R*)args.Pw + (size_t)pid * args.pw_stride;  // (written only when live)
-  CostPipe<M, DIAG, R, G> fwdp{&S, Cg, cg, T, lane, +1};
-  CostPipe<M, DIAG, R, G> bwdp{&S, Cg, cg, T, lane, -1, nullptr, nullptr, Pw};
-  CostPipe<M, DIAG, R, G> lsp{&S, Cg, cg, T, lane, +1, Kw, Kb, Pw};
+  constexpr int FNB = Lay::NB;
+  CostPipe<M, DIAG, R, G, FNB> fwdp{&S, Cg, cg, T, lane, +1};
+  CostPipe<M, DIAG, R, G, FNB> bwdp{&S, Cg, cg, T, lane, -1, nullptr, nullptr, Pw};
+  CostPipe<M, DIAG, R, G, FNB> lsp{&S, Cg, cg, T, lane, +1, Kw, Kb, Pw};
 
   // ---- parameters (prepared: raw + reciprocals), kept in shared memory ----
   const R* thg = (const R*)args.theta + (size_t)args.theta_stride * pid;

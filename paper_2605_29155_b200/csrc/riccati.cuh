@@ -183,9 +183,10 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
 // direction (-1 backward sweeps, +1 forward rollouts). With `Kg` set, the stage's
 // feedback gains K_t (NU padded rows, written by this group's Riccati sweep into the
 // L2-resident gain workspace) ride along as 16-byte cp.async.cg copies into `Kb`.
-template <class M, bool DIAG, class R, int G>
+template <class M, bool DIAG, class R, int G, int NB = Dims<M, DIAG, R>::NBUF>
 struct CostPipe {
   using D = Dims<M, DIAG, R>;
+  // NB stage buffers: the caller provides NB contiguous records at S->Rb (NB >= NB)
   static constexpr int KCH = D::NU * D::LDA * (int)sizeof(R) / 16;  // 16-byte chunks of K_t
   const Ric<M, DIAG, R>* S;
   const R* Cg;
@@ -196,7 +197,7 @@ struct CostPipe {
   const R* Pk = nullptr;  // packed stage records [C_t padded rows | c_t padded] (REC elements)
   static constexpr int REC = D::REC;
   static constexpr int NCH = REC * (int)sizeof(R) / 16;  // 16-byte chunks per record
-  DMPC_DEV int buf(int t) const { return D::NBUF == 2 ? (t & 1) : 0; }
+  DMPC_DEV int buf(int t) const { return NB == 2 ? (t & 1) : 0; }
   DMPC_DEV void issue(int t) {
     if (Pk) {  // contiguous record -> contiguous buffer: fully unrolled 16-byte copies
       const char* src = (const char*)(Pk + (size_t)t * REC) + 16 * lane;
@@ -223,7 +224,7 @@ struct CostPipe {
   DMPC_DEV void start(int t0) { issue(t0); }
   DMPC_DEV void acquire(int t) {
     const int tn = t + step;
-    if (D::NBUF == 2 && tn >= 0 && tn < T) {
+    if (NB == 2 && tn >= 0 && tn < T) {
       issue(tn);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
@@ -232,7 +233,7 @@ struct CostPipe {
   }
   DMPC_DEV void release(int t) {
     const int tn = t + step;
-    if (D::NBUF == 1 && tn >= 0 && tn < T) issue(tn);
+    if (NB == 1 && tn >= 0 && tn < T) issue(tn);
   }
   // write the resident (padded) C_t / c_t out as packed record t (16-byte stores); later
   // sweeps stage it back with plain 16-byte copies
