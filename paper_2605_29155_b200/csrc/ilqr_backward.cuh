@@ -127,14 +127,19 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   }
   {
     const R* xg = (const R*)args.X + (size_t)pid * (T + 1) * NX;
-    for (int e = lane; e < (T + 1) * NX; e += G) {
-      const int t = e / NX, i = e % NX;
-      Xs[t * LDA + i] = xg[e];
-      // the seeds dL/dX, dL/dU are parked in dX / dU (free until the differential
-      // rollout) so the sweep reads them from shared memory, not global
-      dXs[t * LDA + i] = sXg ? sXg[e] : R(0);
+    // lane i takes column i of every row (rows unrolled for the compile-time horizon: all
+    // the loads are in flight at once instead of one global latency per element)
+#pragma unroll 11
+    for (int t = 0; t <= T; t++) {
+      for (int i = lane; i < NX; i += G) {
+        Xs[t * LDA + i] = xg[t * NX + i];
+        // the seeds dL/dX, dL/dU are parked in dX / dU (free until the differential
+        // rollout) so the sweep reads them from shared memory, not global
+        dXs[t * LDA + i] = sXg ? sXg[t * NX + i] : R(0);
+      }
     }
     const R* ug = (const R*)args.U + (size_t)pid * T * NU;
+#pragma unroll 4
     for (int e = lane; e < T * NU; e += G) {
       const R v = ug[e];
       const int t = e / NU, r = e % NU;

@@ -269,10 +269,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   // ---- load x0, U_warm (clipped, ilqr.py:165); zero K, k (Workspace init) ----
   {
     const R* xg = (const R*)args.x0 + (size_t)pid * NX;
-    #pragma unroll 1
     for (int e = lane; e < NX; e += G) Xn[e] = (double)xg[e];
     const R* ug = (const R*)args.U_warm + (size_t)pid * T * NU;
-    #pragma unroll 1
+#pragma unroll 4
     for (int e = lane; e < T * NU; e += G) {
       double v = (double)ug[e];
       const int t = e / NU, r = e % NU;

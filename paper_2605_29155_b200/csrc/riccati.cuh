@@ -150,24 +150,18 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
   if constexpr (DIAG) {
     for (int e = lane; e < D::NZ; e += G) cp_async_elem(dst + e, src + e, pol);
   } else {
-    // element e -> padded (row, col); advanced incrementally (no div/mod per element)
-    int col = lane % D::NZ, off = (lane / D::NZ) * D::ZLD + col;
-#pragma unroll 4
-    for (int e = lane; e < D::NCS; e += G) {
-      cp_async_elem(dst + off, src + e, pol);
-      col += G;
-      off += G;
-      if constexpr (G <= D::NZ) {  // at most one wrap: branch-free select
-        const bool wrap = col >= D::NZ;
-        col = wrap ? col - D::NZ : col;
-        off = wrap ? off + (D::ZLD - D::NZ) : off;
-      } else {
-        while (col >= D::NZ) {
-          col -= D::NZ;
-          off += D::ZLD - D::NZ;
-        }
-      }
+    // lane c copies column c of every row (compile-time row offsets, no index arithmetic);
+    // the columns beyond the group width are spread over the lanes by row
+    constexpr int NZ = D::NZ, ZLD = D::ZLD, GC = G < NZ ? G : NZ;
+    if (lane < GC) {
+#pragma unroll
+      for (int r = 0; r < NZ; r++) cp_async_elem(dst + r * ZLD + lane, src + r * NZ + lane, pol);
     }
+#pragma unroll
+    for (int c = GC; c < NZ; c++)
+#pragma unroll
+      for (int r0 = 0; r0 < NZ; r0 += G)
+        if (r0 + lane < NZ) cp_async_elem(dst + (r0 + lane) * ZLD + c, src + (r0 + lane) * NZ + c, pol);
   }
   if (cg) {
     const R* s2 = cg + (size_t)t * D::NZ;
