@@ -163,6 +163,21 @@ DMPC_DEV double feedback(double v, const R (&krow)[NX], const double (&x)[NX], c
 
 // TC > 0: the horizon is the compile-time constant TC (args.T == TC), so every shared-memory
 // offset and trip count below is a constant (the bench horizon T=10 is instantiated).
+#ifdef DMPC_FWD_PROF
+// -DDMPC_FWD_PROF (development aid): per-phase clock64 totals of every group, summed into
+// g_fwd_prof (0 setup/claim, 1 initial rollout, 2 sweep, 3 line search, 4 epilogue, 5 outputs)
+__device__ unsigned long long g_fwd_prof[8];
+__device__ unsigned g_fwd_done;
+#define FWD_MARK(k)                                                    \
+  do {                                                                 \
+    const long long n_ = clock64();                                    \
+    if (lane == 0) atomicAdd(&g_fwd_prof[k], (unsigned long long)(n_ - tp_)); \
+    tp_ = n_;                                                          \
+  } while (0)
+#else
+#define FWD_MARK(k)
+#endif
+
 template <class M, int G, bool DIAG, class R, bool LOCK, int TC = 0>
 __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
   using D = Dims<M, DIAG, R>;
@@ -213,6 +228,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     if constexpr (LOCK) return __any_sync(wm, v);
     else return v;
   };
+#ifdef DMPC_FWD_PROF
+  long long tp_ = clock64();
+#endif
   for (int pid_ = claim(); wany(pid_ < args.B); pid_ = claim()) {
   const bool live = !LOCK || pid_ < args.B;
   const int pid = live ? pid_ : 0;  // a group past the end reads problem 0, writes nothing
@@ -365,6 +383,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   if (ahist)
     for (int e = lane; e < args.K_max; e += G) ahist[e] = R(0);
 
+  FWD_MARK(0);
   // =========================== initial rollout (kernels.py:161-178) ===========
   if (live) {
     double xc[NX];
@@ -424,6 +443,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   }
   if (jhist && lane == 0) jhist[0] = (R)J;
 
+  FWD_MARK(1);
   // =============================== iterations ==================================
   int it = 0, passes = 0;
   for (; it < args.K_max && wany(active); it++) {
@@ -590,6 +610,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     cp_async_wait_all();
     __syncwarp(gm);
 
+    FWD_MARK(2);
     // --------------------------- stage 3: line search ---------------------------
     const int slot = lane / LC, j = lane % LC;
     const unsigned smask = (LC == 32) ? 0xffffffffu
@@ -686,6 +707,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       }
     }
 
+    FWD_MARK(3);
     // ------------------------- epilogue (ilqr.py:216-244) -----------------------
     const int act = active;
     if (act) iterations = it + 1;
@@ -785,10 +807,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       active = 0;
     }
     if (jhist && lane == 0) jhist[it + 1] = (R)J;
+    FWD_MARK(4);
   }
   if (jhist && lane == 0)
     for (int e = (LOCK ? passes : it) + 1; e <= args.K_max; e++) jhist[e] = (R)J;
 
+  FWD_MARK(6);
   // ================================ outputs ====================================
   const bool failed = fail_t >= 0 || diverged;
   if (live) {
@@ -829,7 +853,20 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   // so made ~100 of 16384 fixed-work solves differ run to run from their first iteration on,
   // while the write-back it saves is ~240 MB per launch, <2% of HBM time.)
   }  // problem scope
+  FWD_MARK(5);
   }  // persistent loop
+#ifdef DMPC_FWD_PROF
+  if (lane == 0) {
+    const unsigned done = atomicAdd(&g_fwd_done, 1u);
+    if (done + 1 == gridDim.x * (unsigned)args.gpb) {
+      printf("fwd prof (cycles, all groups): setup %llu rollout %llu sweep %llu linesearch %llu epilogue %llu "
+             "outputs %llu after-loop %llu\n", g_fwd_prof[0], g_fwd_prof[1], g_fwd_prof[2], g_fwd_prof[3],
+             g_fwd_prof[4], g_fwd_prof[5], g_fwd_prof[6]);
+      for (int k = 0; k < 8; k++) g_fwd_prof[k] = 0;
+      g_fwd_done = 0;
+    }
+  }
+#endif
 }
 
 }  // namespace dmpc
