@@ -59,6 +59,21 @@ DMPC_DEV void cp_async_16cg(void* dst, const void* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
+// element copy without a cache hint. The hinted 4/8-byte form (cp_async_elem) compiled, in some
+// instantiations, to LDGSTS [R+UR0+imm], desc[UR1] with UR0/UR1 never written in the kernel;
+// in the f64 3x2 linear-model backward that faulted (misaligned shared write / illegal
+// instruction), so the element copies of the staging paths carry no hint.
+template <class T>
+DMPC_DEV void cp_async_elem_nh(T* dst, const T* src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if constexpr (sizeof(T) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+// 16-byte copy bypassing L1 with an L2 eviction-priority hint (data read exactly once)
+DMPC_DEV void cp_async_16cg(void* dst, const void* src, uint64_t pol) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "l"(pol));
+}
 DMPC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 DMPC_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 

@@ -100,7 +100,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   const R* sXg = args.dLdX ? (const R*)args.dLdX + (size_t)pid * (T + 1) * NX : nullptr;
   const R* sUg = args.dLdU ? (const R*)args.dLdU + (size_t)pid * T * NU : nullptr;
   const R sJ = args.dLdJ ? ((const R*)args.dLdJ)[pid] : R(0);
-  CostPipe<M, DIAG, R, G> ricp{&S, Cg, nullptr, T, lane, -1};
+  // the sweep's single pass over the caller's C: aligned block copies, unpadded rows (CLD)
+  constexpr bool kBlk = !DIAG && D::NCS + 16 / (int)sizeof(R) - 1 <= D::NCSP;
+  constexpr int CLD = kBlk ? NZ : ZLD;
+  static_assert(DIAG || D::NCS + 16 / (int)sizeof(R) - 1 <= D::NBUF * D::REC, "dC staging holds the shifted block");
+  CostPipe<M, DIAG, R, G, D::NBUF, kBlk> ricp{&S, Cg, nullptr, T, lane, -1};
   CostPipe<M, DIAG, R, G> adjp{&S, Cg, cg, T, lane, -1};
   const bool want_theta = args.dtheta != nullptr && args.n_theta > 0;
   const bool want_adjoint = want_theta || sJ != R(0);
@@ -203,9 +207,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       }
       ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rows);
       __syncwarp(gm);
-      for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R>(S, Cs, e / NU, e % NU, rows);
+      for (int e = lane; e < NU * NU; e += G) S.Quu[(e / NU) * LDB + e % NU] = ric_Quu_entry<M, DIAG, R, CLD>(S, Cs, e / NU, e % NU, rows);
       R quxc[RPL][NU], qxx[RPL][NX];
-      ric_Qxx_Qux<M, DIAG, R, G, RPL>(S, Cs, lane, qxx, quxc, dt_r, rows);
+      ric_Qxx_Qux<M, DIAG, R, G, RPL, CLD>(S, Cs, lane, qxx, quxc, dt_r, rows);
       __syncwarp(gm);
       ricp.release(t);
       // freeze clamped dimensions (kernels.py:658-667)
@@ -366,13 +370,17 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         // order); only the (NZ-G)^2 corner is formed separately -- no second pass of all G
         // lanes for the NZ - G rows beyond the group width
         constexpr int NE = (!DIAG && NZ > G) ? NZ - G : 0;
+        // the block is assembled in the (free) cost staging buffer at the alignment offset of
+        // its global destination, so the copy-out below moves aligned 16-byte chunks
+        R* blk = (!DIAG && dCo) ? dCo + (size_t)t * NZ * NZ : nullptr;
+        R* Rd = S.Rb + (kBlk && blk ? blk_off(blk) : 0);
 #pragma unroll
         for (int ce = 0; ce < NE * NE; ce++) {
           const int r = G + ce / (NE > 0 ? NE : 1), q = G + ce % (NE > 0 ? NE : 1);
           if (dCo && lane == ce % G) {
             const bool cq = clr[q], crr = clr[r];
             const R v = (crr || cq) ? R(0) : R(0.5) * (mul_rn(dzr[r], zr[q]) + mul_rn(zr[r], dzr[q]));
-            S.Rb[r * NZ + q] = v + (R(0.5) * sJ * zr[r]) * zr[q];
+            Rd[r * NZ + q] = v + (R(0.5) * sJ * zr[r]) * zr[q];
           }
         }
 #pragma unroll
@@ -394,14 +402,14 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
               } else {
                 // row a of dC_t goes to the (free) cost staging buffer first; the group then
                 // writes the whole NZ x NZ block with consecutive lanes on consecutive words
-                R* row = S.Rb + a * NZ;
+                R* row = Rd + a * NZ;
                 const R hs = R(0.5) * sJ * za;
 #pragma unroll
                 for (int b = 0; b < NZ; b++) {
                   // products rounded separately (no FMA contraction) so dC is exactly symmetric
                   const R v = (ca || clr[b]) ? R(0) : R(0.5) * (mul_rn(da, zr[b]) + mul_rn(za, dzr[b]));
                   row[b] = v + hs * zr[b];
-                  if (b >= G) S.Rb[b * NZ + a] = v + (R(0.5) * sJ * zr[b]) * za;  // mirror into row b
+                  if (b >= G) Rd[b * NZ + a] = v + (R(0.5) * sJ * zr[b]) * za;  // mirror into row b
                 }
               }
             }
@@ -410,10 +418,23 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         if constexpr (!DIAG) {
           if (dCo) {
             __syncwarp(gm);
-            R* blk = dCo + (size_t)t * NZ * NZ;
+            constexpr int N = NZ * NZ, VN = 16 / (int)sizeof(R);
+            if constexpr (!kBlk) {
 #pragma unroll
-            for (int e0 = 0; e0 < NZ * NZ; e0 += G)
-              if (e0 + lane < NZ * NZ) blk[e0 + lane] = S.Rb[e0 + lane];
+              for (int e0 = 0; e0 < N; e0 += G)
+                if (e0 + lane < N) blk[e0 + lane] = Rd[e0 + lane];
+            } else {
+            const int h = (VN - blk_off(blk)) & (VN - 1), nv = (N - h) / VN;
+            using V = std::conditional_t<sizeof(R) == 4, float4, double2>;
+#pragma unroll
+            for (int m = 0; m < (N / VN + G - 1) / G; m++) {
+              const int k = lane + m * G;
+              if (k < nv) *reinterpret_cast<V*>(blk + h + VN * k) = *reinterpret_cast<const V*>(Rd + h + VN * k);
+            }
+            if (lane < h) blk[lane] = Rd[lane];
+            const int e = h + VN * nv + lane;
+            if (lane < VN && e < N) blk[e] = Rd[e];
+            }
           }
         }
       }

@@ -84,7 +84,13 @@ __host__ __device__ constexpr int group_stride(int T, int G) {
 // the sweep / line search then arrives a whole stage ahead instead of half a stage; the
 // 1.4 KB per problem does not change the register-bound occupancy), single in f64 dense
 template <class M, bool DIAG, class R>
-constexpr int fwd_nbuf() { return (DIAG || sizeof(R) == 4) ? 2 : 1; }
+constexpr int fwd_nbuf() {
+#ifdef DMPC_FWD_NB1
+  return DIAG ? 2 : 1;
+#else
+  return (DIAG || sizeof(R) == 4) ? 2 : 1;
+#endif
+}
 
 template <class M, bool DIAG, class R>
 struct FwdLayout {
@@ -179,7 +185,10 @@ __device__ unsigned g_fwd_done;
 #endif
 
 template <class M, int G, bool DIAG, class R, bool LOCK, int TC = 0>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : 3)) : 2) ilqr_forward_kernel(const FwdArgs args) {
+#ifndef DMPC_FWD_MINB
+#define DMPC_FWD_MINB 3
+#endif
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : DMPC_FWD_MINB)) : 2) ilqr_forward_kernel(const FwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD, XLD = D::XLD, ULD = D::ULD;

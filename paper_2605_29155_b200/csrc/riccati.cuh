@@ -146,28 +146,59 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
   using D = Dims<M, DIAG, R>;
   const R* src = Cg + (size_t)t * D::NCS;
   R* dst = S.Cb(buf);
-  const uint64_t pol = l2_evict_first_policy();
   if constexpr (DIAG) {
-    for (int e = lane; e < D::NZ; e += G) cp_async_elem(dst + e, src + e, pol);
+    for (int e = lane; e < D::NZ; e += G) cp_async_elem_nh(dst + e, src + e);
   } else {
     // lane c copies column c of every row (compile-time row offsets, no index arithmetic);
     // the columns beyond the group width are spread over the lanes by row
     constexpr int NZ = D::NZ, ZLD = D::ZLD, GC = G < NZ ? G : NZ;
     if (lane < GC) {
 #pragma unroll
-      for (int r = 0; r < NZ; r++) cp_async_elem(dst + r * ZLD + lane, src + r * NZ + lane, pol);
+      for (int r = 0; r < NZ; r++) cp_async_elem_nh(dst + r * ZLD + lane, src + r * NZ + lane);
     }
 #pragma unroll
     for (int c = GC; c < NZ; c++)
 #pragma unroll
       for (int r0 = 0; r0 < NZ; r0 += G)
-        if (r0 + lane < NZ) cp_async_elem(dst + (r0 + lane) * ZLD + c, src + (r0 + lane) * NZ + c, pol);
+        if (r0 + lane < NZ) cp_async_elem_nh(dst + (r0 + lane) * ZLD + c, src + (r0 + lane) * NZ + c);
   }
   if (cg) {
     const R* s2 = cg + (size_t)t * D::NZ;
     R* d2 = S.cb(buf);
-    for (int e = lane; e < D::NZ; e += G) cp_async_elem(d2 + e, s2 + e, pol);
+    for (int e = lane; e < D::NZ; e += G) cp_async_elem_nh(d2 + e, s2 + e);
   }
+}
+
+// Alignment-preserving block copy of C_t (dense): the NZ x NZ block is copied as it lies in
+// global memory (unpadded rows, pitch NZ) to Cb(buf) + off, off = the block's element offset
+// within a 16-byte chunk, so every aligned 16-byte chunk of the source lands on an aligned
+// chunk here: ~NZ*NZ/VN 16-byte copies instead of NZ*NZ element copies; the <= 2(VN-1) head /
+// tail elements go one by one. Used by the single pass of the backward, whose consumers read
+// the unpadded rows (ric_Qxx_Qux / ric_Quu_entry with CLD = NZ).
+template <class R>
+DMPC_DEV int blk_off(const R* p) {
+  return (int)(((uintptr_t)p / sizeof(R)) & (uintptr_t)(16 / sizeof(R) - 1));
+}
+template <class M, bool DIAG, class R, int G>
+DMPC_DEV void stage_cost_blk(const Ric<M, DIAG, R>& S, const R* Cg, int t, int buf, int lane) {
+  using D = Dims<M, DIAG, R>;
+  static_assert(!DIAG, "dense cost blocks only");
+  constexpr int N = D::NCS, VN = 16 / (int)sizeof(R);
+  static_assert(N + VN - 1 <= D::NCSP, "staging buffer holds the shifted block");
+  const R* src = Cg + (size_t)t * N;
+  const int off = blk_off(src);
+  const int h = (VN - off) & (VN - 1);  // head elements before the first aligned chunk
+  const int nv = (N - h) / VN;          // aligned chunks
+  R* dst = S.Cb(buf) + off;
+  const uint64_t pol = l2_evict_first_policy();
+#pragma unroll
+  for (int m = 0; m < (N / VN + G - 1) / G; m++) {
+    const int k = lane + m * G;
+    if (k < nv) cp_async_16cg(dst + h + VN * k, src + h + VN * k, pol);
+  }
+  if (lane < h) cp_async_elem_nh(dst + lane, src + lane);
+  const int e = h + VN * nv + lane;
+  if (lane < VN && e < N) cp_async_elem_nh(dst + e, src + e);
 }
 
 // Software pipeline over the per-stage cost tensors: `acquire(t)` makes C_t resident
@@ -177,7 +208,7 @@ DMPC_DEV void stage_cost_t(const Ric<M, DIAG, R>& S, const R* Cg, const R* cg, i
 // direction (-1 backward sweeps, +1 forward rollouts). With `Kg` set, the stage's
 // feedback gains K_t (NU padded rows, written by this group's Riccati sweep into the
 // L2-resident gain workspace) ride along as 16-byte cp.async.cg copies into `Kb`.
-template <class M, bool DIAG, class R, int G, int NB = Dims<M, DIAG, R>::NBUF>
+template <class M, bool DIAG, class R, int G, int NB = Dims<M, DIAG, R>::NBUF, bool BLK = false>
 struct CostPipe {
   using D = Dims<M, DIAG, R>;
   // NB stage buffers: the caller provides NB contiguous records at S->Rb (NB >= NB)
@@ -199,6 +230,8 @@ struct CostPipe {
 #pragma unroll
       for (int k = 0; k < (NCH + G - 1) / G; k++)
         if (k * G + lane < NCH) cp_async_16cg(dst + 16 * G * k, src + 16 * G * k);
+    } else if constexpr (BLK) {
+      stage_cost_blk<M, DIAG, R, G>(*S, Cg, t, buf(t), lane);
     } else {
       stage_cost_t<M, DIAG, R, G>(*S, Cg, cg, t, buf(t), lane);
     }
@@ -238,7 +271,11 @@ struct CostPipe {
     for (int k = 0; k < (NCH + G - 1) / G; k++)
       if (k * G + lane < NCH) d[G * k] = sr[G * k];
   }
-  DMPC_DEV const R* C(int t) const { return S->Cb(buf(t)); }
+  // BLK: unpadded rows (pitch NZ) starting at the staged block's alignment offset
+  DMPC_DEV const R* C(int t) const {
+    if constexpr (BLK) return S->Cb(buf(t)) + blk_off(Cg + (size_t)t * D::NCS);
+    else return S->Cb(buf(t));
+  }
   DMPC_DEV const R* c(int t) const { return S->cb(buf(t)); }
   DMPC_DEV const R* K(int t) const { return Kb + buf(t) * D::NU * D::LDM; }  // rows of LDM
 };
@@ -373,7 +410,8 @@ DMPC_DEV void ric_MA_NB(const Ric<M, DIAG, R>& S, int lane, const R (&vxx)[RPL][
 // C_ux[:,a] + sum_r B[r,:] MA[r,a] (kernels.py:428-433). A' V_xx A is evaluated as
 // MA' A (V_xx is exactly symmetric), i.e. row a = sum_r MA[r,a] A[r,:]: the lane-uniform
 // operand is again a row of A, so its structural zeros are skipped without divergence.
-template <class M, bool DIAG, class R, int G, int RPL, class Rows>
+// CLD: row pitch of the staged C_t (padded ZLD, or NZ for the backward's unpadded block)
+template <class M, bool DIAG, class R, int G, int RPL, int CLD = Dims<M, DIAG, R>::ZLD, class Rows>
 DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&qxx)[RPL][M::NX],
                           R (&quxc)[RPL][M::NU], R dt, const Rows& rows) {
   using D = Dims<M, DIAG, R>;
@@ -390,9 +428,14 @@ DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&q
 #pragma unroll
       for (int i = 0; i < NU; i++) quxc[k][i] = R(0);
     } else {
-      lds_row<NX>(Cs + ac[k] * D::ZLD, qxx[k]);
+      if constexpr (CLD == D::ZLD) {
+        lds_row<NX>(Cs + ac[k] * D::ZLD, qxx[k]);
+      } else {  // unaligned row: scalar loads
 #pragma unroll
-      for (int i = 0; i < NU; i++) quxc[k][i] = Cs[(NX + i) * D::ZLD + ac[k]];
+        for (int bb = 0; bb < NX; bb++) qxx[k][bb] = Cs[ac[k] * CLD + bb];
+      }
+#pragma unroll
+      for (int i = 0; i < NU; i++) quxc[k][i] = Cs[(NX + i) * CLD + ac[k]];
     }
   }
 #pragma unroll
@@ -416,7 +459,7 @@ DMPC_DEV void ric_Qxx_Qux(const Ric<M, DIAG, R>& S, const R* Cs, int lane, R (&q
 }
 
 // Q_uu entry (i,j) = C_uu[i,j] + sum_r B[r,i] NB[r,j]  (kernels.py:434-439)
-template <class M, bool DIAG, class R, class Rows>
+template <class M, bool DIAG, class R, int CLD = Dims<M, DIAG, R>::ZLD, class Rows>
 DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j, const Rows& rows) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX;
@@ -424,7 +467,7 @@ DMPC_DEV R ric_Quu_entry(const Ric<M, DIAG, R>& S, const R* Cs, int i, int j, co
   if constexpr (DIAG) {
     s = (i == j) ? Cs[NX + i] : R(0);
   } else {
-    s = Cs[(NX + i) * D::ZLD + NX + j];
+    s = Cs[(NX + i) * CLD + NX + j];
   }
 #pragma unroll
   for (int r = 0; r < NX; r++)
