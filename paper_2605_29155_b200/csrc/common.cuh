@@ -34,21 +34,6 @@ DMPC_DEV void cp_async_elem(float* dst, const float* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
 }
-// Streaming variants: the caller's cost tensors are read once per stage, so their L2 lines
-// are marked evict-first (they must not push the resident per-problem workspace out).
-DMPC_DEV uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
-DMPC_DEV void cp_async_elem(float* dst, const float* src, uint64_t pol) {
-  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "l"(pol));
-}
-DMPC_DEV void cp_async_elem(double* dst, const double* src, uint64_t pol) {
-  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "l"(pol));
-}
 DMPC_DEV void cp_async_elem(double* dst, const double* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
@@ -68,11 +53,6 @@ DMPC_DEV void cp_async_elem_nh(T* dst, const T* src) {
   unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   if constexpr (sizeof(T) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
   else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
-}
-// 16-byte copy bypassing L1 with an L2 eviction-priority hint (data read exactly once)
-DMPC_DEV void cp_async_16cg(void* dst, const void* src, uint64_t pol) {
-  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "l"(pol));
 }
 DMPC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 DMPC_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }

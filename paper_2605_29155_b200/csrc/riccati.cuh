@@ -190,11 +190,12 @@ DMPC_DEV void stage_cost_blk(const Ric<M, DIAG, R>& S, const R* Cg, int t, int b
   const int h = (VN - off) & (VN - 1);  // head elements before the first aligned chunk
   const int nv = (N - h) / VN;          // aligned chunks
   R* dst = S.Cb(buf) + off;
-  const uint64_t pol = l2_evict_first_policy();
+  // (no L2 cache hint: the hinted forms compiled, in some instantiations, to LDGSTS with a
+  // descriptor register the kernel never writes -- tools/sass_desc_check.py)
 #pragma unroll
   for (int m = 0; m < (N / VN + G - 1) / G; m++) {
     const int k = lane + m * G;
-    if (k < nv) cp_async_16cg(dst + h + VN * k, src + h + VN * k, pol);
+    if (k < nv) cp_async_16cg(dst + h + VN * k, src + h + VN * k);
   }
   if (lane < h) cp_async_elem_nh(dst + lane, src + lane);
   const int e = h + VN * nv + lane;
