@@ -71,7 +71,7 @@ extern "C" {
 /* Problem description (host struct, passed by pointer). Mirrors SolveSettings
  * (ilqr.py:30-60) + DynModel (dynamics.py:32-99). */
 typedef struct DiffMPCProblem {
-  int32_t B;               /* batch size (>= 0; 0 is a no-op)                          */
+  int32_t B;               /* batch size (>= 0; 0 is a no-op, array pointers may be NULL) */
   int32_t T;               /* horizon (>= 1)                                           */
   int32_t nx, nu;          /* state / control dims                                     */
   int32_t model_kind;      /* DIFFMPC_KIND_*                                           */

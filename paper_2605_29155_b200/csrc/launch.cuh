@@ -88,10 +88,10 @@ inline size_t fwd_workspace_bytes(int B, int T, int nx, int nu, int elem, bool d
 template <class M, int G, bool DIAG, class R>
 int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s) {
   if (check_theta<M>(p)) return -1;
-  if (!io || !io->X || !io->U || !io->J || !io->C || !io->c || !io->x0 || !io->U_warm ||
-      (M::NTH > 0 && !io->theta))
+  if (!io) return fail("forward: null io");
+  if (p->B == 0) return 0;  // empty batch: nothing to launch (empty arrays may be NULL)
+  if (!io->X || !io->U || !io->J || !io->C || !io->c || !io->x0 || !io->U_warm || (M::NTH > 0 && !io->theta))
     return fail("forward: required pointer is NULL");
-  if (p->B == 0) return 0;
   FwdArgs a;
   memset(&a, 0, sizeof a);
   a.B = p->B; a.T = p->T; a.K_max = p->K_max; a.n_alpha = p->n_alpha;
@@ -197,10 +197,11 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
 template <class M, int G, bool DIAG, class R>
 int bwd_impl(const DiffMPCProblem* p, const DiffMPCBackwardIO* io, cudaStream_t s) {
   if (check_theta<M>(p)) return -1;
-  if (!io || !io->C || !io->X || !io->U || !io->dc || (M::NTH > 0 && !io->theta))
+  if (!io) return fail("backward: null io");
+  if (p->B == 0) return 0;  // empty batch: nothing to launch (empty arrays may be NULL)
+  if (!io->C || !io->X || !io->U || !io->dc || (M::NTH > 0 && !io->theta))
     return fail("backward: required pointer is NULL");
   if ((io->dtheta || io->dLdJ) && !io->c) return fail("backward: c is required for dtheta / dL/dJ");
-  if (p->B == 0) return 0;
   BwdArgs a;
   memset(&a, 0, sizeof a);
   a.B = p->B; a.T = p->T; a.theta_stride = p->theta_stride; a.n_theta = p->n_theta; a.dt = p->dt;

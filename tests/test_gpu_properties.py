@@ -266,3 +266,21 @@ def test_small_odd_batches_repeatable(B):
     for _ in range(25):
         o = solver.solve_raw(m, pb.settings, pb.x0, C, pb.c, pb.U_warm, kernel="throughput")
         assert torch.equal(o.iters, ref.iters) and torch.equal(o.U, ref.U) and torch.equal(o.J, ref.J)
+
+
+@pytest.mark.parametrize("kernel", ["throughput", "latency"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_empty_batch(kernel, dtype):
+    """B = 0 (an empty minibatch): the forward and the backward return empty outputs of the
+    right shapes and launch nothing (the reference's batch loops simply do not run)."""
+    m = DynModel.quadrotor()
+    pb = problems.random_problem(m, 2, 10, seed=4)
+    z = lambda a: np.asarray(a)[:0]  # noqa: E731
+    n0 = _lib.launch_count()
+    out = solver.solve_raw(m, pb.settings, z(pb.x0), z(pb.dense_C()), z(pb.c), z(pb.U_warm), dtype=dtype,
+                           kernel=kernel)
+    g = solver.backward_raw(m, pb.settings, out.C, out.c, out.X, out.U, None, np.zeros((0, 10, 4)), dtype=dtype)
+    torch.cuda.synchronize()
+    assert _lib.launch_count() == n0
+    assert tuple(out.X.shape) == (0, 11, 13) and tuple(out.U.shape) == (0, 10, 4) and out.J.numel() == 0
+    assert tuple(g.dC.shape) == (0, 10, 17, 17) and tuple(g.dc.shape) == (0, 10, 17) and g.dx0.numel() == 0
