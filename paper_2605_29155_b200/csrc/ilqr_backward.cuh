@@ -313,13 +313,27 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     __syncwarp(gm);
     for (int e = lane; e < NX; e += G) dXs[e] = R(0);  // dX_0 = 0 (seeds no longer needed)
     __syncwarp(gm);
+    // Models with register-resident Jacobian rows (JacRegs) propagate dx_{t+1} = A_t dx_t +
+    // B_t du_t in registers: every lane forms the whole vector from compile-time rows (the
+    // structural zeros skipped, the same FMA order as the row products over the shared copy,
+    // so the values are bit-identical) -- no shared-memory A_t / B_t rewrite and reload per
+    // stage, and dx stays in registers for the next stage.
+    constexpr bool kRegJ = has_jac_regs<M>::value && !M::kLinearParams;
+    R dxc[NX];
+#pragma unroll
+    for (int i = 0; i < NX; i++) dxc[i] = R(0);  // dX_0 = 0
     for (int t = 0; t < T; t++) {
       R xr[NX], ur[NU];
       lds_row<NX>(Xs + t * LDA, xr);
       lds_row<NU>(Us + t * LDB, ur);
-      if constexpr (!M::kLinearParams) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, D::LDM, S.Bs, LDB);
+      if constexpr (!M::kLinearParams && !kRegJ) M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, D::LDM, S.Bs, LDB);
       R dx[NX];
-      lds_row<NX>(dXs + t * LDA, dx);
+      if constexpr (kRegJ) {
+#pragma unroll
+        for (int i = 0; i < NX; i++) dx[i] = dxc[i];
+      } else {
+        lds_row<NX>(dXs + t * LDA, dx);
+      }
       for (int r = lane; r < NU; r += G) {
         R s = ka[t * LDB + r];
         R krow[NX];
@@ -331,8 +345,42 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       __syncwarp(gm);
       R du[NU];
       lds_row<NU>(dUs + t * LDB, du);
+      if constexpr (kRegJ) {
+        R z[NZ];
 #pragma unroll
-      for (int k = 0; k < RPL; k++) {
+        for (int i = 0; i < NX; i++) z[i] = xr[i];
+#pragma unroll
+        for (int i = 0; i < NU; i++) z[NX + i] = ur[i];
+        RegRows<M, R> rows;
+        M::template jac_regs<R>(P_r, dt_r, z, rows.J);
+#pragma unroll
+        for (int a = 0; a < NX; a++) {
+          R arow[NX], brow[NU];
+          rows.get(a, arow, brow);
+          R s = R(0);
+#pragma unroll
+          for (int b = 0; b < NX; b++) {
+            if (M::a_one(a, b)) s += dx[b];
+            else if (M::a_dt(a, b)) s += dt_r * dx[b];
+            else if (M::a_nz(a, b)) s += arow[b] * dx[b];
+          }
+#pragma unroll
+          for (int b = 0; b < NU; b++)
+            if (M::b_nz(a, b)) s += brow[b] * du[b];
+          dxc[a] = s;
+        }
+        // the lane's entries of dX_{t+1} (rows a = lane + k G) for the assembly and the output
+#pragma unroll
+        for (int k = 0; k < RPL; k++) {
+          R own = dxc[k * G];
+#pragma unroll
+          for (int l = 1; l < G; l++)
+            if (k * G + l < NX) own = (lane == l) ? dxc[k * G + l] : own;
+          if (k * G + lane < NX) dXs[(t + 1) * LDA + k * G + lane] = own;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < (kRegJ ? 0 : RPL); k++) {
         const int a = row_of<G, RPL>(lane, k);
         if (a < NX) {
           R arow[NX], brow[NU];
