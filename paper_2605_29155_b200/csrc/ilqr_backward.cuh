@@ -182,28 +182,69 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       // stage Jacobian values once (register rows + the shared copy for column accesses)
       using Rows = std::conditional_t<has_jac_regs<M>::value, RegRows<M, R>, SmemRows<M, DIAG, R>>;
       Rows rows = make_rows<M, DIAG, R>(S, P_r, dt_r, zr);
-      if constexpr (has_jac_regs<M>::value) {
-        jac_store_rows<M, R>(rows, S.As, D::LDM, S.Bs, LDB);
-      } else if constexpr (!M::kLinearParams) {
+      constexpr bool kRegJ = has_jac_regs<M>::value;
+      if constexpr (!kRegJ && !M::kLinearParams) {
         M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, D::LDM, S.Bs, LDB);
+        __syncwarp(gm);
       }
-      __syncwarp(gm);
       R qx[RPL];
       R vx[NX];
       lds_row<NX>(S.Vx, vx);
+      if constexpr (kRegJ) {
+        // A'Vx / B'Vx from the register rows (as in the forward sweep): every lane forms each
+        // column's chain from its own seed, in the shared-copy products' order with the
+        // structural zeros skipped (bit-identical), and keeps the column it owns
 #pragma unroll
-      for (int k = 0; k < RPL; k++) {
-        const int a = min(row_of<G, RPL>(lane, k), NX - 1);
-        R s = dXs[t * LDA + a];
+        for (int k = 0; k < RPL; k++) {
+          const int a = min(row_of<G, RPL>(lane, k), NX - 1);
+          const R seed = dXs[t * LDA + a];
+          R own = seed;
 #pragma unroll
-        for (int b2 = 0; b2 < NX; b2++) s += S.As[b2 * D::LDM + a] * vx[b2];
-        qx[k] = s;
-      }
-      for (int a = lane; a < NU; a += G) {
-        R s = dUs[t * LDB + a];
+          for (int cc = 0; cc < NX; cc++) {
+            R e = seed;
 #pragma unroll
-        for (int b2 = 0; b2 < NX; b2++) s += S.Bs[b2 * LDB + a] * vx[b2];
-        S.qu[a] = s;
+            for (int b2 = 0; b2 < NX; b2++) {
+              if (!M::a_nz(b2, cc)) continue;
+              R arow[NX], brow[NU];
+              rows.get(b2, arow, brow);
+              if (M::a_one(b2, cc)) e += vx[b2];
+              else if (M::a_dt(b2, cc)) e += dt_r * vx[b2];
+              else e += arow[cc] * vx[b2];
+            }
+            own = a == cc ? e : own;
+          }
+          qx[k] = own;
+        }
+        static_assert(!kRegJ || NU <= G, "one lane per control component");
+        {
+          const int a = lane < NU ? lane : 0;
+          const R seed = dUs[t * LDB + a];
+          R own = seed;
+#pragma unroll
+          for (int cc = 0; cc < NU; cc++) {
+            R e = seed;
+#pragma unroll
+            for (int b2 = 0; b2 < NX; b2++)
+              if (b_row_nz<M>(b2)) e += rows.b(b2, cc) * vx[b2];
+            own = a == cc ? e : own;
+          }
+          if (lane < NU) S.qu[a] = own;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < RPL; k++) {
+          const int a = min(row_of<G, RPL>(lane, k), NX - 1);
+          R s = dXs[t * LDA + a];
+#pragma unroll
+          for (int b2 = 0; b2 < NX; b2++) s += S.As[b2 * D::LDM + a] * vx[b2];
+          qx[k] = s;
+        }
+        for (int a = lane; a < NU; a += G) {
+          R s = dUs[t * LDB + a];
+#pragma unroll
+          for (int b2 = 0; b2 < NX; b2++) s += S.Bs[b2 * LDB + a] * vx[b2];
+          S.qu[a] = s;
+        }
       }
       ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rows);
       __syncwarp(gm);

@@ -488,8 +488,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       // of the state-dependent entries for the column accesses (A'Vx, B'NB)
       using Rows = std::conditional_t<has_jac_regs<M>::value, RegRows<M, R>, SmemRows<M, DIAG, R>>;
       Rows rows = make_rows<M, DIAG, R>(S, P_r, dt_r, zv);
-      if constexpr (has_jac_regs<M>::value) {
-        jac_store_rows<M, R>(rows, S.As, D::LDM, S.Bs, LDB);
+      constexpr bool kRegJ = has_jac_regs<M>::value;
+      if constexpr (kRegJ) {
+        // A'Vx / B'Vx below are formed from the register rows: no shared copy needed
       } else if constexpr (!M::kLinearParams) {
         R xr[NX], ur[NU];
 #pragma unroll
@@ -498,10 +499,47 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         for (int i = 0; i < NU; i++) ur[i] = zv[NX + i];
         M::template jac_vary<R>(P_r, dt_r, xr, ur, S.As, D::LDM, S.Bs, LDB);
       }
-      __syncwarp(gm);
+      if constexpr (!kRegJ) __syncwarp(gm);
       // gz = C z + c ; qx = gz_x + A' Vx ; qu = gz_u + B' Vx   (kernels.py:395-410)
       R qx[RPL];
       lds_row<NX>(S.Vx, vx);
+      // Register rows: column c of A' Vx as the same two FMA chains (even / odd rows b2, in
+      // order, structural zeros skipped: +0 terms) the shared-copy products below form, so
+      // the values are bit-identical; each lane keeps the columns it owns (selects).
+      R avx[RPL][2], bvx[2];
+      if constexpr (kRegJ) {
+#pragma unroll
+        for (int k = 0; k < RPL; k++) avx[k][0] = avx[k][1] = R(0);
+        bvx[0] = bvx[1] = R(0);
+#pragma unroll
+        for (int cc = 0; cc < NX; cc++) {
+          R e[2] = {R(0), R(0)};
+#pragma unroll
+          for (int b2 = 0; b2 < NX; b2++) {
+            if (!M::a_nz(b2, cc)) continue;
+            R arow[NX], brow[NU];
+            rows.get(b2, arow, brow);
+            if (M::a_one(b2, cc)) e[b2 & 1] += vx[b2];
+            else if (M::a_dt(b2, cc)) e[b2 & 1] += dt_r * vx[b2];
+            else e[b2 & 1] += arow[cc] * vx[b2];
+          }
+#pragma unroll
+          for (int k = 0; k < RPL; k++) {
+            const int a = min(row_of<G, RPL>(lane, k), NX - 1);
+            avx[k][0] = a == cc ? e[0] : avx[k][0];
+            avx[k][1] = a == cc ? e[1] : avx[k][1];
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < NU; cc++) {
+          R e[2] = {R(0), R(0)};
+#pragma unroll
+          for (int b2 = 0; b2 < NX; b2++)
+            if (b_row_nz<M>(b2)) e[b2 & 1] += rows.b(b2, cc) * vx[b2];
+          bvx[0] = lane == cc ? e[0] : bvx[0];
+          bvx[1] = lane == cc ? e[1] : bvx[1];
+        }
+      }
 #pragma unroll
       for (int k = 0; k < RPL; k++) {
         const int a = min(row_of<G, RPL>(lane, k), NX - 1);
@@ -514,8 +552,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
 #pragma unroll
           for (int b2 = 0; b2 < NZ; b2++) sa[b2 & 1] += crow[b2] * zv[b2];
         }
+        if constexpr (kRegJ) {
+          sa[2] = avx[k][0];
+          sa[3] = avx[k][1];
+        } else {
 #pragma unroll
-        for (int b2 = 0; b2 < NX; b2++) sa[2 + (b2 & 1)] += S.As[b2 * D::LDM + a] * vx[b2];
+          for (int b2 = 0; b2 < NX; b2++) sa[2 + (b2 & 1)] += S.As[b2 * D::LDM + a] * vx[b2];
+        }
         qx[k] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
       }
       for (int a = lane; a < NU; a += G) {
@@ -528,9 +571,14 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
 #pragma unroll
           for (int b2 = 0; b2 < NZ; b2++) sa[b2 & 1] += crow[b2] * zv[b2];
         }
+        if constexpr (kRegJ) {
+          sa[2] = bvx[0];
+          sa[3] = bvx[1];
+        } else {
 #pragma unroll
-        for (int b2 = 0; b2 < NX; b2++)
-          if (b_row_nz<M>(b2)) sa[2 + (b2 & 1)] += S.Bs[b2 * LDB + a] * vx[b2];
+          for (int b2 = 0; b2 < NX; b2++)
+            if (b_row_nz<M>(b2)) sa[2 + (b2 & 1)] += S.Bs[b2 * LDB + a] * vx[b2];
+        }
         S.qu[a] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
       }
       ric_MA_NB<M, DIAG, R, G, RPL>(S, lane, vxx, dt_r, rows);
