@@ -110,7 +110,8 @@ struct FwdLayout {
     o = align_up(o, 16);
     L.oKb = o; o += NB * D::NU * D::LDM * (int)sizeof(R);
     o = align_up(o, 16);
-    L.ric = RicLayout<M, DIAG, R>::make(o);
+    // models with register-resident Jacobian rows never read a shared A_t / B_t copy here
+    L.ric = RicLayout<M, DIAG, R>::make(o, !(has_jac_regs<M>::value && !M::kLinearParams));
     // the record buffers are the last array of the Riccati scratch: extra ones follow it
     L.total = align_up(L.ric.end + (NB - D::NBUF) * D::REC * (int)sizeof(R), 16);
     return L;
@@ -188,7 +189,10 @@ template <class M, int G, bool DIAG, class R, bool LOCK, int TC = 0>
 #ifndef DMPC_FWD_MINB
 #define DMPC_FWD_MINB 3
 #endif
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : DMPC_FWD_MINB)) : 2) ilqr_forward_kernel(const FwdArgs args) {
+#ifndef DMPC_FWD_MAXT
+#define DMPC_FWD_MAXT 128
+#endif
+__global__ void __launch_bounds__(DMPC_FWD_MAXT, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 ? 4 : DMPC_FWD_MINB)) : 2) ilqr_forward_kernel(const FwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD, XLD = D::XLD, ULD = D::ULD;
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   if constexpr (M::kLinearParams) {
     for (int e = lane; e < NX * NX; e += G) S.As[(e / NX) * D::LDM + e % NX] = thg[e];
     for (int e = lane; e < NX * NU; e += G) S.Bs[(e / NU) * LDB + e % NU] = thg[NX * NX + e];
-  } else {
+  } else if constexpr (!has_jac_regs<M>::value) {
     M::template jac_const<R>(P_r, dt_r, S.As, D::LDM, S.Bs, LDB, lane, G);
   }
 

@@ -105,12 +105,14 @@ template <class M, bool DIAG, class R>
 struct RicLayout {
   using D = Dims<M, DIAG, R>;
   int oAs, oBs, oMA, oNB, oKT, oQuu, oqu, oVx, ozs, oR, end;
-  __host__ __device__ static constexpr RicLayout make(int o) {
+  // ab = false: no shared copy of A_t / B_t (a kernel that takes every Jacobian entry from
+  // registers; As / Bs then alias the next array and must not be touched)
+  __host__ __device__ static constexpr RicLayout make(int o, bool ab = true) {
     RicLayout L{};
     const int s = (int)sizeof(R);
     auto take = [&](int n) { int r = o; o = rup(o + n * s, 16); return r; };
-    L.oAs = take(D::NX * D::LDM);
-    L.oBs = take(D::NX * D::LDB);
+    L.oAs = take(ab ? D::NX * D::LDM : 0);
+    L.oBs = take(ab ? D::NX * D::LDB : 0);
     L.oMA = take(D::NX * D::LDM);
     L.oNB = take(D::NX * D::LDB);
     L.oKT = take(D::NX * D::LDB);
