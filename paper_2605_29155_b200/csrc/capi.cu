@@ -4,6 +4,7 @@
 // compiled (model, n_x, n_u) instantiation, sizes the launch (problems per block
 // from the shared-memory footprint) and enqueues exactly ONE kernel per call on the
 // caller's stream. Nothing here synchronises the stream.
+#include <mutex>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -58,6 +59,28 @@ int num_sms() {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 1;
   }
   return v;
+}
+
+cudaMemPool_t work_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[128] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      cudaGetLastError();
+      cudaDeviceGetDefaultMemPool(&pools[dev], dev);
+    } else {
+      uint64_t keep = UINT64_MAX;  // never trim: a per-call workspace is reused at no cost
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+  return pools[dev];
 }
 
 int max_smem_optin() {

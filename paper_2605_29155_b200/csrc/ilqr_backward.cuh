@@ -36,12 +36,23 @@ struct BwdArgs {
   void* dX;
   void* dU;
   int32_t* fail_t;
+  void* Kg;  // lean layout: auxiliary gain workspace (B, T, NU, LDA) of R
+  int ab;    // lean layout: the A_t / B_t region past each group's block is allocated
 };
+
+// Lean layout (models with register-resident Jacobian rows): the auxiliary gains K live in
+// an L2 workspace (written by the sweep, streamed back one stage ahead by the rollout into
+// two small staging buffers) and the shared A_t / B_t copy, which only the co-state
+// recursions still use, sits past the end of the group's block and is allocated only when
+// the call wants them (dtheta or dL/dJ): 9.2 -> 5.9 KB per 13-state problem, 4 blocks per SM.
+template <class M>
+constexpr bool bwd_lean() { return has_jac_regs<M>::value && !M::kLinearParams; }
 
 template <class M, bool DIAG, class R>
 struct BwdLayout {
   using D = Dims<M, DIAG, R>;
-  int oPr, oX, oU, oK, ok, odX, odU, ocl, olam, olh, total;
+  static constexpr bool kLean = bwd_lean<M>();
+  int oPr, oX, oU, oK, ok, odX, odU, ocl, olam, olh, oAB, total, total_ab;
   RicLayout<M, DIAG, R> ric;
   __host__ __device__ static constexpr BwdLayout make(int T) {
     BwdLayout L{};
@@ -51,22 +62,27 @@ struct BwdLayout {
     L.oPr = take(M::NP * s);
     L.oX = take((T + 1) * D::LDA * s);
     L.oU = take(T * D::LDB * s);
-    L.oK = take(T * D::NU * D::LDA * s);
+    L.oK = take((kLean ? 2 : T) * D::NU * D::LDA * s);
     L.ok = take(T * D::LDB * s);
     L.odX = take((T + 1) * D::LDA * s);
     L.odU = take(T * D::LDB * s);
     L.ocl = take(T * D::NU);
     L.olam = take(D::LDA * s);
     L.olh = take(D::LDA * s);
-    L.ric = RicLayout<M, DIAG, R>::make(o);
+    L.ric = RicLayout<M, DIAG, R>::make(o, !kLean);
     L.total = align_up(L.ric.end, 16);
+    L.oAB = L.total;
+    L.total_ab = kLean ? align_up(L.total + (D::NX * D::LDM + D::NX * D::LDB) * s, 16) : L.total;
     return L;
   }
 };
 
 // TC > 0: compile-time horizon (args.T == TC): constant shared-memory offsets (see the forward)
+#ifndef DMPC_BWD_MINB
+#define DMPC_BWD_MINB 3
+#endif
 template <class M, int G, bool DIAG, class R, int TC = 0>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 || DIAG ? 4 : 3)) : 2) ilqr_backward_kernel(const BwdArgs args) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2 : (M::NX <= 8 || DIAG || bwd_lean<M>() ? 4 : DMPC_BWD_MINB)) : 2) ilqr_backward_kernel(const BwdArgs args) {
   using D = Dims<M, DIAG, R>;
   constexpr int NX = M::NX, NU = M::NU, NZ = NX + NU;
   constexpr int LDA = D::LDA, LDB = D::LDB, ZLD = D::ZLD;
@@ -81,7 +97,8 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   const unsigned gm = group_mask<G>();
   const int T = TC > 0 ? TC : args.T;
   const Lay L = Lay::make(T);
-  const int sstride = TC > 0 ? group_stride<Lay>(TC, G) : args.smem_stride;
+  constexpr bool kLean = Lay::kLean;
+  const int sstride = (TC > 0 && !kLean) ? group_stride<Lay>(TC, G) : args.smem_stride;
   unsigned char* base = smem_raw + (size_t)grp * sstride;
   R* Xs = (R*)(base + L.oX);    // rows of LDA
   R* Us = (R*)(base + L.oU);    // rows of LDB
@@ -94,6 +111,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   R* lhs = (R*)(base + L.olh);
   Ric<M, DIAG, R> S;
   S.bind(base, L.ric);
+  if constexpr (kLean) {  // (only touched when args.ab: the co-state recursions)
+    S.As = (R*)(base + L.oAB);
+    S.Bs = S.As + D::NX * D::LDM;
+  }
+  R* const Kgp = kLean ? (R*)args.Kg + (size_t)pid * T * NU * LDA : nullptr;
 
   const R* Cg = (const R*)args.C + (size_t)pid * T * D::NCS;
   const R* cg = args.c ? (const R*)args.c + (size_t)pid * T * NZ : nullptr;
@@ -126,7 +148,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
   if constexpr (M::kLinearParams) {
     for (int e = lane; e < NX * NX; e += G) S.As[(e / NX) * D::LDM + e % NX] = thg[e];
     for (int e = lane; e < NX * NU; e += G) S.Bs[(e / NU) * LDB + e % NU] = thg[NX * NX + e];
-  } else {
+  } else if (!kLean || args.ab) {
     M::template jac_const<R>(P_r, dt_r, S.As, D::LDM, S.Bs, LDB, lane, G);
   }
   {
@@ -306,7 +328,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
         for (int i = 0; i < NU; i++) kcol[k][i] = -sol[i];
         if (b2 < NX) {
 #pragma unroll
-          for (int i = 0; i < NU; i++) Ka[(t * NU + i) * LDA + b2] = kcol[k][i];
+          for (int i = 0; i < NU; i++) (kLean ? Kgp : Ka)[(t * NU + i) * LDA + b2] = kcol[k][i];
           ric_publish_cols<M, DIAG, R>(S, b2, kcol[k], quxc[k], true);
           R s = qx[k];
 #pragma unroll
@@ -363,7 +385,27 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
     R dxc[NX];
 #pragma unroll
     for (int i = 0; i < NX; i++) dxc[i] = R(0);  // dX_0 = 0
+    // lean layout: K_t arrives from the L2 workspace one stage ahead (16-byte copies into
+    // the two staging buffers at Ka)
+    constexpr int KCH = NU * LDA * (int)sizeof(R) / 16;
+    auto issue_k = [&](int t) {
+#pragma unroll
+      for (int c0 = 0; c0 < KCH; c0 += G)
+        if (c0 + lane < KCH)
+          cp_async_16cg((char*)(Ka + (t & 1) * NU * LDA) + 16 * (c0 + lane), (const char*)(Kgp + (size_t)t * NU * LDA) + 16 * (c0 + lane));
+      cp_async_commit();
+    };
+    if constexpr (kLean) {
+      __threadfence_block();  // the sweep's gain stores before the group's copies of them
+      __syncwarp(gm);
+      issue_k(0);
+    }
     for (int t = 0; t < T; t++) {
+      if constexpr (kLean) {
+        cp_async_wait_all();
+        __syncwarp(gm);  // K_t resident; every lane done with the buffer K_{t+1} goes to
+        if (t + 1 < T) issue_k(t + 1);
+      }
       R xr[NX], ur[NU];
       lds_row<NX>(Xs + t * LDA, xr);
       lds_row<NU>(Us + t * LDB, ur);
@@ -378,7 +420,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? (G == 4 && M::NX > 8 ? 2
       for (int r = lane; r < NU; r += G) {
         R s = ka[t * LDB + r];
         R krow[NX];
-        lds_row<NX>(Ka + (t * NU + r) * LDA, krow);
+        lds_row<NX>(Ka + (kLean ? ((t & 1) * NU + r) : (t * NU + r)) * LDA, krow);
 #pragma unroll
         for (int b = 0; b < NX; b++) s += krow[b] * dx[b];
         dUs[t * LDB + r] = s;

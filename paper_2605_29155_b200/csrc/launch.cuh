@@ -17,6 +17,9 @@ namespace dmpc {
 int fail(const char* fmt, ...) __attribute__((format(printf, 1, 2)));
 extern std::atomic<int64_t> g_launches;
 int max_smem_optin();
+// the library's stream-ordered pool for internal workspaces (current device; memory is kept
+// cached across calls instead of going back to the driver at every synchronisation)
+cudaMemPool_t work_pool();
 
 // default lanes per problem (a lane owns ceil(n_x / G) state rows)
 constexpr int default_group(int nx) { return nx <= 4 ? 4 : (nx <= 8 ? 8 : 16); }
@@ -32,12 +35,13 @@ int check_theta(const DiffMPCProblem* p) {
 // Problems per block: among gpb in {128/G, 64/G, 32/G, ...} pick the one that keeps the
 // most problems resident per SM (occupancy API: registers + shared memory).
 template <class Lay, class K>
-int plan(K kern, int B, int T, int G, int& gpb, int& stride, int* per_sm = nullptr) {
+int plan(K kern, int B, int T, int G, int& gpb, int& stride, int* per_sm = nullptr, int bytes = 0) {
   const Lay L = Lay::make(T);
   // per-group stride = whole 128-byte lines + G banks: the 32/G groups of a warp start G
   // banks apart, so a warp-wide access of consecutive elements (lane = row or column
   // index, one per group) covers all 32 banks instead of hitting the same 16 twice
-  stride = group_stride<Lay>(T, G);
+  // (`bytes` > 0: the group's block size when it differs from Lay::make(T).total)
+  stride = bytes > 0 ? (bytes + 127) / 128 * 128 + 4 * G : group_stride<Lay>(T, G);
   (void)L;
   const int limit = max_smem_optin();
   int best = -1, best_res = -1;
@@ -175,7 +179,8 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
   void* ws = io->workspace;
   bool own = false;
   if (!ws || io->workspace_bytes < wsb) {
-    if (cudaMallocAsync(&ws, wsb, s) != cudaSuccess) return fail("forward: workspace allocation of %zu bytes failed", wsb);
+    if (cudaMallocFromPoolAsync(&ws, wsb, work_pool(), s) != cudaSuccess)
+      return fail("forward: workspace allocation of %zu bytes failed", wsb);
     own = true;
   }
   const size_t gs = fwd_gain_stride(p->T, M::NX, M::NU, (int)sizeof(R));
@@ -216,11 +221,22 @@ int bwd_impl(const DiffMPCProblem* p, const DiffMPCBackwardIO* io, cudaStream_t 
   if constexpr (sizeof(R) == 4) {
     if (p->T == 10) kern = ilqr_backward_kernel<M, G, DIAG, R, 10>;
   }
-  if (plan<BwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride)) return -1;
+  using BL = BwdLayout<M, DIAG, R>;
+  const BL bl = BL::make(p->T);
+  a.ab = (io->dtheta != nullptr && p->n_theta > 0) || io->dLdJ != nullptr;  // co-state recursions
+  if (plan<BL>(kern, p->B, p->T, G, a.gpb, a.smem_stride, nullptr, a.ab ? bl.total_ab : bl.total)) return -1;
   const int smem = a.gpb * a.smem_stride;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int blocks = (p->B + a.gpb - 1) / a.gpb;
+  void* kw = nullptr;
+  if constexpr (BL::kLean) {  // auxiliary gain workspace, stream-ordered
+    const size_t kb = (size_t)p->B * p->T * M::NU * Dims<M, DIAG, R>::LDA * sizeof(R);
+    if (cudaMallocFromPoolAsync(&kw, kb, work_pool(), s) != cudaSuccess)
+      return fail("backward: gain workspace allocation of %zu bytes failed", kb);
+    a.Kg = kw;
+  }
   kern<<<blocks, a.gpb * G, smem, s>>>(a);
+  if (kw) cudaFreeAsync(kw, s);
   g_launches.fetch_add(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail("backward launch failed: %s", cudaGetErrorString(e));
