@@ -92,11 +92,18 @@ constexpr int fwd_nbuf() {
 #endif
 }
 
-template <class M, bool DIAG, class R>
+template <class M, bool DIAG, class R, bool LOCK = false>
 struct FwdLayout {
   using D = Dims<M, DIAG, R>;
   static constexpr int NB = fwd_nbuf<M, DIAG, R>();
-  int oPe, oPr, oXn, oUn, oUs, okg, oKb, total;
+  // kXs: the alpha_0 line-search candidate writes its states to a second state buffer (the
+  // shared memory the register-Jacobian models no longer spend on A_t / B_t) instead of over
+  // the nominal, so a rejected alpha_0 needs no restoring re-roll. Measured (B=16384, T=10,
+  // dense f32): fixed work 3.18 -> 2.82 ms, random costs 2.52 -> 2.46 ms, but the hover batch
+  // 0.892 -> 0.900 ms (the extra 1.2 KB per problem); so only the warp-lockstep schedule
+  // (fixed-work solves, long horizons) uses it.
+  static constexpr bool kXs = LOCK && has_jac_regs<M>::value && !M::kLinearParams;
+  int oPe, oPr, oXn, oXs, oUn, oUs, okg, oKb, total;
   RicLayout<M, DIAG, R> ric;
   __host__ __device__ static constexpr FwdLayout make(int T) {
     FwdLayout L{};
@@ -104,6 +111,7 @@ struct FwdLayout {
     L.oPe = o; o += align_up(M::NP * 8, 16);
     L.oPr = o; o += align_up(M::NP * (int)sizeof(R), 16);
     L.oXn = o; o += (T + 1) * D::XLD * 8;
+    L.oXs = o; o += kXs ? (T + 1) * D::XLD * 8 : 0;
     L.oUn = o; o += T * D::ULD * 8;
     L.oUs = o; o += T * D::ULD * 8;
     L.okg = o; o += T * D::ULD * 8;
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(DMPC_FWD_MAXT, sizeof(R) == 4 ? (G == 4 && M::
   constexpr int RPL = (NX + G - 1) / G;  // state rows owned by each lane
   constexpr int NSLOT = G >= 4 ? 4 : G;  // concurrent line-search candidates
   constexpr int LC = G / NSLOT;          // lanes per candidate slot
-  using Lay = FwdLayout<M, DIAG, R>;
+  using Lay = FwdLayout<M, DIAG, R, LOCK>;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
@@ -211,7 +219,9 @@ __global__ void __launch_bounds__(DMPC_FWD_MAXT, sizeof(R) == 4 ? (G == 4 && M::
   const Lay L = Lay::make(T);
   const int sstride = TC > 0 ? group_stride<Lay>(TC, G) : args.smem_stride;
   unsigned char* base = smem_raw + (size_t)grp * sstride;
-  double* const Xn = (double*)(base + L.oXn);
+  constexpr bool kXs = Lay::kXs;
+  double* Xn = (double*)(base + L.oXn);  // nominal states (kXs: swapped with Xs on accept)
+  double* Xs = kXs ? (double*)(base + L.oXs) : Xn;
   double* const Ubuf0 = (double*)(base + L.oUn);
   double* const Ubuf1 = (double*)(base + L.oUs);
   double* kg = (double*)(base + L.okg);
@@ -725,7 +735,7 @@ __global__ void __launch_bounds__(DMPC_FWD_MAXT, sizeof(R) == 4 ? (G == 4 && M::
             u[r] = (LC == 1) ? urr[r] : __shfl_sync(smask, urr[r / LC], (lane & ~(LC - 1)) + (r % LC), G);
           Jm += stage_cost(std::integral_constant<int, LC>{}, lsp.C(t), lsp.c(t), xc, u, j, smask);
           __syncwarp(gm);  // every slot has read the nominal X_t
-          if (shadow) store_owned<NX, LC>(Xn + t * XLD, xc, j);
+          if (shadow) store_owned<NX, LC>(Xs + t * XLD, xc, j);
           lsp.release(t);
           double xn[NX];
           step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xc, u, xn);
@@ -739,7 +749,7 @@ __global__ void __launch_bounds__(DMPC_FWD_MAXT, sizeof(R) == 4 ? (G == 4 && M::
         // per-stage tests, decided once per candidate
 #pragma unroll
         for (int i = 0; i < NX; i++) dm |= !finite_(xc[i]);
-        if (shadow) store_owned<NX, LC>(Xn + T * XLD, xc, j);
+        if (shadow) store_owned<NX, LC>(Xs + T * XLD, xc, j);
         cp_async_wait_all();
         // one reduction per candidate; a non-finite stage cost leaves a non-finite sum
         Jm = sum_lanes(std::integral_constant<int, LC>{}, Jm, smask);
@@ -775,14 +785,17 @@ __global__ void __launch_bounds__(DMPC_FWD_MAXT, sizeof(R) == 4 ? (G == 4 && M::
     const bool all_dead = act && alld;
     const bool accept = act && !all_dead && (best_J < J);
     if (ahist && lane == 0) ahist[it] = accept ? (R)args.alphas[best] : R(0);
-    const bool inplace_used = act && inplace;  // the nominal X now holds alpha_0's states
+    const bool inplace_used = act && inplace;  // alpha_0's states are in Xs (== X unless kXs)
     if (accept && best == 0 && inplace_used) {
-      // adopt the alpha_0 candidate: its states are already in X, its controls in Us
+      // adopt the alpha_0 candidate: its states are in Xs, its controls in Us
       __syncwarp(gm);
       double* tu = Un; Un = Us; Us = tu;
-    } else if (accept || inplace_used) {
+      if constexpr (kXs) {
+        double* tx = Xn; Xn = Xs; Xs = tx;
+      }
+    } else if (accept || (!kXs && inplace_used)) {
       // Re-roll the nominal (xb, bit-identical to the rollout that produced it: restores X
-      // after alpha_0 overwrote it) and, on accept, the winning candidate (xw, bit-identical
+      // after alpha_0 overwrote it; kXs: X is intact and xb is read from it) and, on accept, the winning candidate (xw, bit-identical
       // to its line-search pass), adopting the latter. Writes to X_t / U_t are delayed until
       // every lane has read the old U_t.
       const double alpha = args.alphas[best];
@@ -840,9 +853,13 @@ __global__ void __launch_bounds__(DMPC_FWD_MAXT, sizeof(R) == 4 ? (G == 4 && M::
             if (lane + m2 * G < NU) Un[t * ULD + lane + m2 * G] = v[m2];
         }
         double xn[NX];
-        step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xb, ub, xn);
+        if constexpr (kXs) {  // the nominal is intact (alpha_0 wrote to Xs): read, not re-rolled
+          lds_row_d<NX>(Xn + (t + 1) * XLD, xb);
+        } else {
+          step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xb, ub, xn);
 #pragma unroll
-        for (int i = 0; i < NX; i++) xb[i] = xn[i];
+          for (int i = 0; i < NX; i++) xb[i] = xn[i];
+        }
         if (accept) {
           step_e<M, R>(P_e, dt_e, S.As, D::LDM, S.Bs, LDB, xw, uw, xn);
 #pragma unroll

@@ -152,7 +152,9 @@ int fwd_impl(const DiffMPCProblem* p, const DiffMPCForwardIO* io, cudaStream_t s
     }
   }
   int per_sm = 1;
-  if (plan<FwdLayout<M, DIAG, R>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)) return -1;
+  if ((lock ? plan<FwdLayout<M, DIAG, R, true>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)
+            : plan<FwdLayout<M, DIAG, R, false>>(kern, p->B, p->T, G, a.gpb, a.smem_stride, &per_sm)))
+    return -1;
   if (const char* e = getenv("DIFFMPC_GPB")) {  // tuning override (even, keeps warps full)
     const int g = atoi(e);
     if (g >= 2 && g % 2 == 0 && g * G <= 128 && g * a.smem_stride <= max_smem_optin()) {  // launch bounds: 128 threads
