@@ -78,6 +78,11 @@ cudaMemPool_t work_pool() {
     } else {
       uint64_t keep = UINT64_MAX;  // never trim: a per-call workspace is reused at no cost
       cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+      // no hidden cross-stream waits: a call on one stream must not be made to wait for the
+      // release point of a workspace freed on another (pipelined streams would serialise);
+      // the pool grows by one workspace per concurrently active stream instead
+      int no = 0;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolReuseAllowInternalDependencies, &no);
     }
   }
   return pools[dev];
