@@ -210,14 +210,23 @@ def run_ours(args):
         return out, g
 
     # ---- device-resident timing (value) ----
+    # Through a SolvePlan (the library's preallocated launch path: outputs, gradients and the
+    # workspace allocated once, each call patches the input pointers and enqueues the kernel):
+    # the same two kernels per step, with ~10x less host work per call than solve_raw, so a
+    # slow or contended host cannot starve the GPU between the timed launches.
+    plan = solver.SolvePlan(model, st, B, layout=args.layout, dtype=dtype, device=dev)
+
+    def pstep():
+        o = plan.solve(dev_in["x0"], dev_in["C"], dev_in["c"], dev_in["U_warm"])
+        return o, plan.backward(None, dev_in["dLdU"])
+
     clk = ClockSampler(local).__enter__()  # sample clocks from warm-up through the timed region
     for _ in range(args.warmup):
-        out, g = step(dev_in)
+        out, g = pstep()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = _lib.launch_count()
-    iters_all = []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -230,12 +239,10 @@ def run_ours(args):
                 flush.zero_()
             e0, e1, e2 = ev[k]
             e0.record(stream)
-            out = solver.solve_raw(model, st, dev_in["x0"], dev_in["C"], dev_in["c"], dev_in["U_warm"], dtype=dtype)
+            out = plan.solve(dev_in["x0"], dev_in["C"], dev_in["c"], dev_in["U_warm"])
             e1.record(stream)
-            g = solver.backward_raw(model, st, dev_in["C"], dev_in["c"], out.X, out.U, None, dev_in["dLdU"],
-                                    dtype=dtype)
+            g = plan.backward(None, dev_in["dLdU"])
             e2.record(stream)
-            iters_all.append(out.iters)
         t_end.record(stream)
         torch.cuda.synchronize()
     clk.__exit__(None, None, None)
@@ -250,8 +257,8 @@ def run_ours(args):
         elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / args.steps
     value = world * B / (ms_per_step * 1e-3)
-    iters = torch.stack(iters_all).float()
-    it_np = iters_all[-1].cpu().numpy()
+    iters = out.iters.float()  # (identical inputs every step: the last step's counts)
+    it_np = out.iters.cpu().numpy()
 
     # ---- end-to-end through the public API with pinned host buffers ----
     # Every step copies its inputs host->device, solves + differentiates, and copies the
